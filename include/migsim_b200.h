@@ -1,0 +1,120 @@
+/*
+ * migsim-b200: C-ABI of the B200 batched engine for the reference's replica hot path.
+ *
+ * The reference evaluates its multi-tenancy controller by fanning (variant, seed) replicas of
+ * `engine::run_scenario` out over std::async threads
+ *   - replica entry  : RunResult run_scenario(const ScenarioSpec&, const RunOptions&)
+ *                      /root/reference/proj/include/migsim/engine.hpp:117 (impl engine.cpp:898-902)
+ *   - fan-out        : harness::run_plan, /root/reference/proj/src/harness.cpp:156-176
+ *   - scenario input : scenario-v1 YAML, /root/reference/proj/src/scenario.cpp:322-374
+ * This ABI replaces that fan-out with one batched GPU call.  Plain C types only; all buffers are
+ * caller-owned except results, which are freed with migsim_batch_result_free.  No exceptions
+ * cross the ABI.  Calls are synchronous; one handle per host thread.
+ *
+ * Return codes: 0 ok; 1 config error (message carries "file:line" like model::ConfigError,
+ * model.hpp:29-37); 2 runtime/CUDA error; 3 parity guard (a device-sized buffer would have
+ * truncated; nothing is silently dropped).
+ */
+#ifndef MIGSIM_B200_H
+#define MIGSIM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MIGSIM_API __attribute__((visibility("default")))
+#else
+#define MIGSIM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MIGSIM_OK 0
+#define MIGSIM_ERR_CONFIG 1
+#define MIGSIM_ERR_RUNTIME 2
+#define MIGSIM_ERR_PARITY_GUARD 3
+
+typedef struct migsim_gpu migsim_gpu;
+typedef struct migsim_batch_result migsim_batch_result;
+
+/* harness::Variant (harness.hpp:40-46) plus the e3 sweep knobs (harness.cpp:89-110).
+ * Integer flags: -1 keeps the scenario's value. */
+typedef struct migsim_variant {
+    const char* name;
+    int32_t enabled, enable_mig, enable_placement, enable_guardrails;
+    double sample_interval_s;   /* <= 0: keep */
+    int32_t persistence_windows; /* <= 0: keep */
+    int32_t dwell_obs;           /* <= 0: keep */
+    int32_t cooldown_obs;        /* < 0: keep  */
+    int32_t validation_obs;      /* <= 0: keep */
+} migsim_variant;
+
+/* engine::RunOptions (engine.hpp:94-99) batch form. */
+typedef struct migsim_run_opts {
+    int32_t keep_completions;   /* store per-completion records (parity/debug; memory heavy) */
+    int32_t max_wave_replicas;  /* 0: sized from free device memory */
+    int32_t action_cap;         /* per-replica action-log capacity, 0: default 1024 */
+    int32_t pause_cap;          /* per-replica pause-log capacity, 0: default 1024 */
+} migsim_run_opts;
+
+/* device-side timing of the last batch (CUDA events on the batch stream), milliseconds */
+typedef struct migsim_timing {
+    double gen_ms, des_ms, select_ms, total_device_ms, wall_ms;
+    int64_t replicas, tenant_ticks, completions, arrivals, events, waves;
+    int64_t select_samples;  /* measurement-window latencies fed to the select kernel */
+} migsim_timing;
+
+/* per (run, tenant) flat summary row, tenants in lexicographic id order
+ * (engine::TenantSummary, engine.hpp:67-78, plus p999) */
+typedef struct migsim_tenant_row {
+    uint64_t completed_total, completed_window, window_misses;
+    double mean_ms, p50_ms, p95_ms, p99_ms, p999_ms, miss_rate, throughput_hz;
+} migsim_tenant_row;
+
+MIGSIM_API int migsim_gpu_open(int device, migsim_gpu** out, char* err, size_t errlen);
+MIGSIM_API void migsim_gpu_close(migsim_gpu* g);
+
+/* scenario::parse_scenario / load_scenario (scenario.hpp:65-68) */
+MIGSIM_API int migsim_gpu_load_scenario(migsim_gpu* g, const char* yaml_text, const char* source_name, int32_t* scenario_id,
+                             char* err, size_t errlen);
+MIGSIM_API int migsim_gpu_load_scenario_file(migsim_gpu* g, const char* path, int32_t* scenario_id, char* err, size_t errlen);
+/* canonical tenant order of a loaded scenario: writes the i-th id (lexicographic) */
+MIGSIM_API int migsim_scenario_n_tenants(migsim_gpu* g, int32_t scenario_id);
+MIGSIM_API int migsim_scenario_tenant_id(migsim_gpu* g, int32_t scenario_id, int32_t i, char* buf, size_t buflen);
+
+/* variants x seeds replicas, row-major (variant-major, seed-minor) like harness.cpp:125-152 */
+MIGSIM_API int migsim_gpu_run_batch(migsim_gpu* g, int32_t scenario_id, const migsim_variant* variants, size_t n_variants,
+                         const uint64_t* seeds, size_t n_seeds, const migsim_run_opts* opts,
+                         migsim_batch_result** out, char* err, size_t errlen);
+
+MIGSIM_API size_t migsim_batch_n_runs(const migsim_batch_result* r);
+MIGSIM_API int migsim_batch_n_tenants(const migsim_batch_result* r);
+MIGSIM_API int migsim_batch_timing(const migsim_batch_result* r, migsim_timing* t);
+/* rows [n_runs * n_tenants] */
+MIGSIM_API int migsim_batch_tenant_rows(const migsim_batch_result* r, migsim_tenant_row* rows, size_t cap);
+/* full engine::RunResult of one run as JSON (summary + actions + pauses + stability);
+ * the pointer stays valid until the result is freed */
+MIGSIM_API const char* migsim_batch_run_json(migsim_batch_result* r, size_t run);
+/* per-completion records of one run (only with keep_completions): 7 doubles per completion
+ * {tenant, seq, done_s, total_ms, compute_ms, transfer_ms, noise_ms}, tenant-major order */
+MIGSIM_API int64_t migsim_batch_completions(const migsim_batch_result* r, size_t run, double* out, int64_t cap);
+MIGSIM_API void migsim_batch_result_free(migsim_batch_result* r);
+
+/* Standalone nearest-rank select (telemetry.cpp:38-56 / engine.cpp:800-816 semantics) over
+ * n_segments host segments vals[seg_off[s] .. seg_off[s+1]); out[s * n_q + j] = quantile qs[j]. */
+MIGSIM_API int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off, size_t n_segments, const double* qs,
+                      size_t n_q, double* out, double* device_ms, char* err, size_t errlen);
+
+/* Batched experiment plans (harness::run_plan, harness.cpp:114-216): plan in {e1,e2,e3,llm};
+ * returns experiment.json (same keys/aggregation: population-sigma CIs in seed order). */
+MIGSIM_API int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, int32_t seeds, uint64_t seed_base,
+                    const char* focus_tenant, char** experiment_json, char* err, size_t errlen);
+MIGSIM_API void migsim_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MIGSIM_B200_H */

@@ -175,9 +175,7 @@ MG_HD double tw_quantile(TailWin& w, double q) {
         tw_rebuild(w);
         return w.top[j];
     }
-    // generic fallback (q far below the tail): gather and select
-    double tmp_unused = 0.0;
-    (void)tmp_unused;
+    // generic fallback (q far below the tail): selection over the ring in place
     double best = 0.0;
     {
         // selection over the ring in place

@@ -19,12 +19,13 @@
 
 #include <stdint.h>
 
+#include <cmath>
+#include <cstring>
+
 #if defined(__CUDACC__)
 #define MG_HD __host__ __device__ __forceinline__
 #else
 #define MG_HD inline
-#include <cmath>
-#include <cstring>
 #endif
 
 namespace mg {

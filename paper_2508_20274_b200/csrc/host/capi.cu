@@ -1,0 +1,710 @@
+// C-ABI of the B200 engine (include/migsim_b200.h): scenario loading, wave-batched replica
+// execution on one GPU, result assembly, the standalone select, and batched experiment plans.
+// There is no CPU execution path: every replica runs in the CUDA kernels of engine_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/migsim_b200.h"
+#include "../kernels/engine_kernels.cuh"
+#include "packer.hpp"
+#include "result_json.hpp"
+
+namespace mg {
+size_t select_smem_bytes();
+}
+
+namespace {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ParityGuard : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                          \
+    do {                                                                                               \
+        cudaError_t e_ = (x);                                                                          \
+        if (e_ != cudaSuccess)                                                                         \
+            throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_) + " (" + __FILE__ + ":" + \
+                            std::to_string(__LINE__) + ")");                                           \
+    } while (0)
+
+void set_err(char* err, size_t len, const std::string& msg) {
+    if (!err || len == 0) return;
+    std::snprintf(err, len, "%s", msg.c_str());
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        return MIGSIM_OK;
+    } catch (const mgb::ConfigError& e) {
+        set_err(err, errlen, e.what());
+        return MIGSIM_ERR_CONFIG;
+    } catch (const ParityGuard& e) {
+        set_err(err, errlen, e.what());
+        return MIGSIM_ERR_PARITY_GUARD;
+    } catch (const std::exception& e) {
+        set_err(err, errlen, e.what());
+        return MIGSIM_ERR_RUNTIME;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count) CK(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+};
+
+}  // namespace
+
+struct migsim_gpu {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[6] = {};
+    std::vector<mgb::ScenarioSpec> scenarios;
+};
+
+struct migsim_batch_result {
+    mgb::ScenarioSpec spec;
+    mgb::Packed P;
+    std::vector<mgb::Variant> variants;
+    std::vector<uint64_t> seeds;
+    size_t n_runs = 0;
+    int T = 0, R = 0;
+    std::vector<mg::TenantOut> tout;
+    std::vector<double> quant;
+    std::vector<mg::ReplicaOut> rout;
+    std::vector<double> backlog;
+    std::vector<mg::ActionRec> actions;
+    std::vector<int64_t> act_off;
+    std::vector<mg::PauseRec> pauses;
+    std::vector<int64_t> pause_off;
+    std::vector<double> comps;
+    std::vector<int64_t> comp_off;
+    std::vector<std::string> json;
+    migsim_timing timing{};
+};
+
+namespace {
+
+struct WaveAlloc {
+    DevBuf<double> arr_t, arr_bytes, arr_mult, arr_noise, irq_e, t_all, req_ms, win_lat;
+    DevBuf<double> c_done, c_total, c_compute, c_transfer, c_noise;
+    DevBuf<int32_t> n_all, n_kept, variant, gen_overflow, file_order;
+    DevBuf<uint64_t> mt_pause, seeds;
+    DevBuf<mg::ActionRec> actions, actions_c;
+    DevBuf<mg::PauseRec> pauses, pauses_c;
+    DevBuf<mg::TenantOut> tout;
+    DevBuf<mg::ReplicaOut> rout;
+    DevBuf<double> backlog, quant, rings;
+    DevBuf<int64_t> off, cap, act_off, pause_off;
+    DevBuf<mg::PScenario> scen;
+    DevBuf<mg::PController> ctrl;
+};
+
+void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vector<mgb::Variant>& variants,
+                    const std::vector<uint64_t>& seeds, const migsim_run_opts& opts, migsim_batch_result& res,
+                    double cap_sigmas, int action_cap, int pause_cap) {
+    const auto wall0 = std::chrono::steady_clock::now();
+    CK(cudaSetDevice(g->device));
+    res.spec = spec;
+    res.variants = variants;
+    res.seeds = seeds;
+    res.P = mgb::pack(spec, variants, cap_sigmas);
+    const mgb::Packed& P = res.P;
+    const int T = P.scen.n_tenants, R = P.scen.n_roots;
+    const size_t n_var = P.ctrl.size();
+    const size_t n_jobs = n_var * seeds.size();
+    res.n_runs = n_jobs;
+    res.T = T;
+    res.R = R;
+    const bool keep = opts.keep_completions != 0;
+    // working-set layout: controller rings in shared memory when a replica stays under 96 KB
+    mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true);
+    const bool rings_in_smem = L.total <= 96 * 1024;
+    if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false);
+    // wave size from free memory
+    const size_t per_rep = static_cast<size_t>(P.cap_sum) * 8 * (8 + (keep ? 5 : 0)) + static_cast<size_t>(T) * 8 +
+                           static_cast<size_t>(T) * mg::kMtN * 8 + static_cast<size_t>(action_cap) * sizeof(mg::ActionRec) * 2 +
+                           static_cast<size_t>(pause_cap) * sizeof(mg::PauseRec) * 2 + T * sizeof(mg::TenantOut) +
+                           sizeof(mg::ReplicaOut) + static_cast<size_t>(R) * 16 + static_cast<size_t>(T) * 32 + 64 +
+                           (rings_in_smem ? 0 : static_cast<size_t>(T) * (P.max_dwell + P.max_validation) * 8);
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    size_t W = std::max<size_t>(1, static_cast<size_t>(0.70 * static_cast<double>(free_b)) / per_rep);
+    if (opts.max_wave_replicas > 0) W = std::min<size_t>(W, static_cast<size_t>(opts.max_wave_replicas));
+    W = std::min(W, n_jobs);
+    if (W == 0) W = 1;
+
+    WaveAlloc A;
+    const size_t big = W * static_cast<size_t>(P.cap_sum);
+    A.arr_t.alloc(big);
+    A.arr_bytes.alloc(big);
+    A.arr_mult.alloc(big);
+    A.arr_noise.alloc(big);
+    A.irq_e.alloc(big);
+    A.t_all.alloc(big);
+    A.req_ms.alloc(big);
+    A.win_lat.alloc(big);
+    if (keep) {
+        A.c_done.alloc(big);
+        A.c_total.alloc(big);
+        A.c_compute.alloc(big);
+        A.c_transfer.alloc(big);
+        A.c_noise.alloc(big);
+    }
+    A.n_all.alloc(W * T);
+    A.n_kept.alloc(W * T);
+    A.variant.alloc(W);
+    A.seeds.alloc(W);
+    A.gen_overflow.alloc(1);
+    A.file_order.alloc(T);
+    A.mt_pause.alloc(W * T * mg::kMtN);
+    A.actions.alloc(W * action_cap);
+    A.actions_c.alloc(W * action_cap);
+    A.pauses.alloc(W * pause_cap);
+    A.pauses_c.alloc(W * pause_cap);
+    A.tout.alloc(W * T);
+    A.rout.alloc(W);
+    A.backlog.alloc(W * R * 2);
+    A.quant.alloc(W * T * 4);
+    if (!rings_in_smem) A.rings.alloc(W * T * (P.max_dwell + P.max_validation));
+    A.off.alloc(T);
+    A.cap.alloc(T);
+    A.act_off.alloc(W + 1);
+    A.pause_off.alloc(W + 1);
+    A.scen.alloc(1);
+    A.ctrl.alloc(n_var);
+    cudaStream_t s = g->stream;
+    CK(cudaMemcpyAsync(A.scen.p, &P.scen, sizeof(mg::PScenario), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(A.ctrl.p, P.ctrl.data(), sizeof(mg::PController) * n_var, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(A.off.p, P.off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(A.cap.p, P.cap.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(A.file_order.p, P.file_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
+
+    mg::WaveBuffers B{};
+    B.arr_t = A.arr_t.p;
+    B.arr_bytes = A.arr_bytes.p;
+    B.arr_mult = A.arr_mult.p;
+    B.arr_noise = A.arr_noise.p;
+    B.irq_e = A.irq_e.p;
+    B.t_all = A.t_all.p;
+    B.req_ms = A.req_ms.p;
+    B.win_lat = A.win_lat.p;
+    B.c_done = A.c_done.p;
+    B.c_total = A.c_total.p;
+    B.c_compute = A.c_compute.p;
+    B.c_transfer = A.c_transfer.p;
+    B.c_noise = A.c_noise.p;
+    B.n_all = A.n_all.p;
+    B.n_kept = A.n_kept.p;
+    B.mt_pause = A.mt_pause.p;
+    B.actions = A.actions.p;
+    B.pauses = A.pauses.p;
+    B.tout = A.tout.p;
+    B.rout = A.rout.p;
+    B.backlog = A.backlog.p;
+    B.quant = A.quant.p;
+    B.rings = A.rings.p;
+    B.seeds = A.seeds.p;
+    B.variant = A.variant.p;
+    B.off = A.off.p;
+    B.cap = A.cap.p;
+    B.file_order = A.file_order.p;
+    B.gen_overflow = A.gen_overflow.p;
+    B.cap_sum = P.cap_sum;
+    B.action_cap = action_cap;
+    B.pause_cap = pause_cap;
+    B.any_irq_noise = P.any_irq_noise;
+    B.rings_in_smem = rings_in_smem;
+    B.dwell = P.max_dwell;
+    B.validation = P.max_validation;
+
+    CK(cudaFuncSetAttribute(mg::des_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+    const size_t sel_smem = mg::select_smem_bytes();
+    CK(cudaFuncSetAttribute(mg::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sel_smem)));
+
+    res.tout.resize(n_jobs * T);
+    res.quant.resize(n_jobs * T * 4);
+    res.rout.resize(n_jobs);
+    res.backlog.resize(n_jobs * R * 2);
+    res.act_off.assign(n_jobs + 1, 0);
+    res.pause_off.assign(n_jobs + 1, 0);
+    if (keep) res.comp_off.assign(n_jobs + 1, 0);
+
+    std::vector<uint64_t> wseeds(W);
+    std::vector<int32_t> wvar(W);
+    std::vector<int64_t> aoff(W + 1), poff(W + 1);
+    std::vector<int32_t> nkept(W * T);
+    double gen_ms = 0, des_ms = 0, sel_ms = 0;
+    int64_t completions = 0, arrivals = 0, events = 0, waves = 0, samples = 0;
+    for (size_t j0 = 0; j0 < n_jobs; j0 += W) {
+        const int w = static_cast<int>(std::min(W, n_jobs - j0));
+        ++waves;
+        for (int k = 0; k < w; ++k) {
+            wseeds[k] = seeds[(j0 + k) % seeds.size()];
+            wvar[k] = static_cast<int32_t>((j0 + k) / seeds.size());
+        }
+        CK(cudaMemcpyAsync(A.seeds.p, wseeds.data(), sizeof(uint64_t) * w, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(A.variant.p, wvar.data(), sizeof(int32_t) * w, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(A.gen_overflow.p, 0, sizeof(int32_t), s));
+        CK(cudaEventRecord(g->ev[0], s));
+        const int64_t nt = static_cast<int64_t>(w) * T;
+        mg::gen_times_kernel<<<static_cast<unsigned>((nt + 127) / 128), 128, 0, s>>>(A.scen.p, B, w);
+        mg::gen_marks_kernel<<<static_cast<unsigned>((4 * nt + 127) / 128), 128, 0, s>>>(A.scen.p, B, w);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g->ev[1], s));
+        mg::des_kernel<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g->ev[2], s));
+        mg::select_kernel<<<static_cast<unsigned>(nt), 256, sel_smem, s>>>(B, T, w);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g->ev[3], s));
+        int32_t overflow = 0;
+        CK(cudaMemcpyAsync(&overflow, A.gen_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(res.rout.data() + j0, A.rout.p, sizeof(mg::ReplicaOut) * w, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(nkept.data(), A.n_kept.p, sizeof(int32_t) * w * T, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (overflow) throw ParityGuard("arrival-record capacity exceeded");
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
+        gen_ms += ms;
+        CK(cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]));
+        des_ms += ms;
+        CK(cudaEventElapsedTime(&ms, g->ev[2], g->ev[3]));
+        sel_ms += ms;
+        aoff[0] = poff[0] = 0;
+        for (int k = 0; k < w; ++k) {
+            const mg::ReplicaOut& ro = res.rout[j0 + k];
+            if (ro.error) throw ParityGuard("device log capacity exceeded (code " + std::to_string(ro.error) + ")");
+            aoff[k + 1] = aoff[k] + ro.n_actions;
+            poff[k + 1] = poff[k] + ro.n_pauses;
+            events += static_cast<int64_t>(ro.n_events);
+        }
+        for (int k = 0; k < w * T; ++k) arrivals += nkept[k];
+        CK(cudaMemcpyAsync(A.act_off.p, aoff.data(), sizeof(int64_t) * (w + 1), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(A.pause_off.p, poff.data(), sizeof(int64_t) * (w + 1), cudaMemcpyHostToDevice, s));
+        mg::compact_actions_kernel<<<static_cast<unsigned>(w), 64, 0, s>>>(A.actions.p, action_cap, A.rout.p, A.act_off.p,
+                                                                           A.actions_c.p, w);
+        mg::compact_pauses_kernel<<<static_cast<unsigned>(w), 64, 0, s>>>(A.pauses.p, pause_cap, A.rout.p, A.pause_off.p,
+                                                                          A.pauses_c.p, w);
+        CK(cudaGetLastError());
+        const size_t a0 = res.actions.size(), p0 = res.pauses.size();
+        res.actions.resize(a0 + static_cast<size_t>(aoff[w]));
+        res.pauses.resize(p0 + static_cast<size_t>(poff[w]));
+        for (int k = 0; k < w; ++k) {
+            res.act_off[j0 + k + 1] = static_cast<int64_t>(a0) + aoff[k + 1];
+            res.pause_off[j0 + k + 1] = static_cast<int64_t>(p0) + poff[k + 1];
+        }
+        if (aoff[w]) CK(cudaMemcpyAsync(res.actions.data() + a0, A.actions_c.p, sizeof(mg::ActionRec) * aoff[w], cudaMemcpyDeviceToHost, s));
+        if (poff[w]) CK(cudaMemcpyAsync(res.pauses.data() + p0, A.pauses_c.p, sizeof(mg::PauseRec) * poff[w], cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(res.tout.data() + j0 * T, A.tout.p, sizeof(mg::TenantOut) * w * T, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(res.quant.data() + j0 * T * 4, A.quant.p, sizeof(double) * w * T * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(res.backlog.data() + j0 * R * 2, A.backlog.p, sizeof(double) * w * R * 2, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int k = 0; k < w * T; ++k) {
+            completions += static_cast<int64_t>(res.tout[j0 * T + k].completed_total);
+            samples += static_cast<int64_t>(res.tout[j0 * T + k].completed_window);
+        }
+        if (keep) {
+            std::vector<double> tmp(static_cast<size_t>(P.cap_sum) * 5);
+            for (int k = 0; k < w; ++k) {
+                const size_t job = j0 + k;
+                const int64_t base = static_cast<int64_t>(k) * P.cap_sum;
+                CK(cudaMemcpy(tmp.data() + 0 * P.cap_sum, A.c_done.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(tmp.data() + 1 * P.cap_sum, A.c_total.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(tmp.data() + 2 * P.cap_sum, A.c_compute.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(tmp.data() + 3 * P.cap_sum, A.c_transfer.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(tmp.data() + 4 * P.cap_sum, A.c_noise.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                for (int i = 0; i < T; ++i) {
+                    const uint64_t n = res.tout[job * T + i].completed_total;
+                    for (uint64_t c = 0; c < n; ++c) {
+                        const int64_t o = P.off[i] + static_cast<int64_t>(c);
+                        const double rec[7] = {static_cast<double>(i), static_cast<double>(c), tmp[o],
+                                               tmp[P.cap_sum + o], tmp[2 * P.cap_sum + o], tmp[3 * P.cap_sum + o],
+                                               tmp[4 * P.cap_sum + o]};
+                        res.comps.insert(res.comps.end(), rec, rec + 7);
+                    }
+                }
+                res.comp_off[job + 1] = static_cast<int64_t>(res.comps.size() / 7);
+            }
+        }
+    }
+    res.json.assign(n_jobs, std::string());
+    res.timing.gen_ms = gen_ms;
+    res.timing.des_ms = des_ms;
+    res.timing.select_ms = sel_ms;
+    res.timing.total_device_ms = gen_ms + des_ms + sel_ms;
+    res.timing.replicas = static_cast<int64_t>(n_jobs);
+    res.timing.tenant_ticks = static_cast<int64_t>(n_jobs) * T * P.scen.n_ticks;
+    res.timing.completions = completions;
+    res.timing.arrivals = arrivals;
+    res.timing.events = events;
+    res.timing.waves = waves;
+    res.timing.select_samples = samples;
+    res.timing.wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+}
+
+mgb::Variant to_variant(const migsim_variant& v) {
+    mgb::Variant o;
+    o.name = v.name ? v.name : "as-is";
+    o.enabled = v.enabled;
+    o.enable_mig = v.enable_mig;
+    o.enable_placement = v.enable_placement;
+    o.enable_guardrails = v.enable_guardrails;
+    o.sample_interval_s = v.sample_interval_s;
+    o.persistence_windows = v.persistence_windows;
+    o.dwell_obs = v.dwell_obs;
+    o.cooldown_obs = v.cooldown_obs;
+    o.validation_obs = v.validation_obs;
+    return o;
+}
+
+void run_batch_checked(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vector<mgb::Variant>& vs,
+                       const std::vector<uint64_t>& seeds, const migsim_run_opts& o, migsim_batch_result& res) {
+    const int acap = o.action_cap > 0 ? o.action_cap : 1024;
+    const int pcap = o.pause_cap > 0 ? o.pause_cap : 1024;
+    try {
+        run_batch_impl(g, spec, vs, seeds, o, res, 12.0, acap, pcap);
+    } catch (const ParityGuard&) {
+        // never truncate: rerun once with much larger device buffers
+        res = migsim_batch_result{};
+        run_batch_impl(g, spec, vs, seeds, o, res, 48.0, acap * 16, pcap * 16);
+    }
+}
+
+// harness.cpp:32-43 (population sigma, summed in seed order)
+void ci(const std::vector<double>& v, double& mean, double& half) {
+    mean = half = 0.0;
+    if (v.empty()) return;
+    const double n = static_cast<double>(v.size());
+    double sum = 0.0;
+    for (double x : v) sum += x;
+    mean = sum / n;
+    double ss = 0.0;
+    for (double x : v) ss += (x - mean) * (x - mean);
+    half = 1.96 * std::sqrt(ss / n) / std::sqrt(n);
+}
+
+std::string num(double v) {
+    char b[40];
+    std::snprintf(b, sizeof(b), "%.17g", v);
+    return b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int migsim_gpu_open(int device, migsim_gpu** out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) throw CudaError("no CUDA device " + std::to_string(device));
+        CK(cudaSetDevice(device));
+        auto* g = new migsim_gpu();
+        g->device = device;
+        CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        for (auto& e : g->ev) CK(cudaEventCreate(&e));
+        *out = g;
+    });
+}
+
+void migsim_gpu_close(migsim_gpu* g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    for (auto& e : g->ev)
+        if (e) cudaEventDestroy(e);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+}
+
+int migsim_gpu_load_scenario(migsim_gpu* g, const char* yaml_text, const char* source_name, int32_t* scenario_id,
+                             char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        g->scenarios.push_back(mgb::parse_scenario(yaml_text, source_name ? source_name : "<scenario>"));
+        *scenario_id = static_cast<int32_t>(g->scenarios.size() - 1);
+    });
+}
+
+int migsim_gpu_load_scenario_file(migsim_gpu* g, const char* path, int32_t* scenario_id, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        g->scenarios.push_back(mgb::load_scenario(path));
+        *scenario_id = static_cast<int32_t>(g->scenarios.size() - 1);
+    });
+}
+
+int migsim_scenario_n_tenants(migsim_gpu* g, int32_t id) {
+    if (!g || id < 0 || id >= static_cast<int32_t>(g->scenarios.size())) return -1;
+    return static_cast<int>(g->scenarios[static_cast<size_t>(id)].tenants.size());
+}
+
+int migsim_scenario_tenant_id(migsim_gpu* g, int32_t id, int32_t i, char* buf, size_t buflen) {
+    if (!g || id < 0 || id >= static_cast<int32_t>(g->scenarios.size())) return MIGSIM_ERR_CONFIG;
+    std::vector<std::string> ids;
+    for (const auto& t : g->scenarios[static_cast<size_t>(id)].tenants) ids.push_back(t.spec.id);
+    std::sort(ids.begin(), ids.end());
+    if (i < 0 || i >= static_cast<int32_t>(ids.size())) return MIGSIM_ERR_CONFIG;
+    std::snprintf(buf, buflen, "%s", ids[static_cast<size_t>(i)].c_str());
+    return MIGSIM_OK;
+}
+
+int migsim_gpu_run_batch(migsim_gpu* g, int32_t scenario_id, const migsim_variant* variants, size_t n_variants,
+                         const uint64_t* seeds, size_t n_seeds, const migsim_run_opts* opts, migsim_batch_result** out,
+                         char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
+            throw mgb::ConfigError("unknown scenario id");
+        if (n_seeds == 0) throw mgb::ConfigError("experiment needs at least one seed");
+        std::vector<mgb::Variant> vs;
+        for (size_t i = 0; i < n_variants; ++i) vs.push_back(to_variant(variants[i]));
+        if (vs.empty()) vs.push_back(mgb::Variant{});
+        migsim_run_opts o{};
+        if (opts) o = *opts;
+        auto res = std::make_unique<migsim_batch_result>();
+        run_batch_checked(g, g->scenarios[static_cast<size_t>(scenario_id)], vs,
+                          std::vector<uint64_t>(seeds, seeds + n_seeds), o, *res);
+        *out = res.release();
+    });
+}
+
+size_t migsim_batch_n_runs(const migsim_batch_result* r) { return r ? r->n_runs : 0; }
+int migsim_batch_n_tenants(const migsim_batch_result* r) { return r ? r->T : 0; }
+
+int migsim_batch_timing(const migsim_batch_result* r, migsim_timing* t) {
+    if (!r || !t) return MIGSIM_ERR_RUNTIME;
+    *t = r->timing;
+    return MIGSIM_OK;
+}
+
+int migsim_batch_tenant_rows(const migsim_batch_result* r, migsim_tenant_row* rows, size_t cap) {
+    if (!r || !rows) return MIGSIM_ERR_RUNTIME;
+    const double window_s = r->spec.duration_s - r->spec.measure_start_s;
+    const size_t n = r->n_runs * static_cast<size_t>(r->T);
+    if (cap < n) return MIGSIM_ERR_RUNTIME;
+    for (size_t k = 0; k < n; ++k) {
+        const mg::TenantOut& o = r->tout[k];
+        migsim_tenant_row& w = rows[k];
+        w.completed_total = o.completed_total;
+        w.completed_window = o.completed_window;
+        w.window_misses = o.window_misses;
+        const double c = static_cast<double>(o.completed_window);
+        w.mean_ms = o.completed_window ? o.sum_total_ms / c : 0.0;
+        w.p50_ms = o.completed_window ? r->quant[4 * k + 0] : 0.0;
+        w.p95_ms = o.completed_window ? r->quant[4 * k + 1] : 0.0;
+        w.p99_ms = o.completed_window ? r->quant[4 * k + 2] : 0.0;
+        w.p999_ms = o.completed_window ? r->quant[4 * k + 3] : 0.0;
+        w.miss_rate = o.completed_window ? static_cast<double>(o.window_misses) / c : 0.0;
+        w.throughput_hz = o.completed_window ? c / window_s : 0.0;
+    }
+    return MIGSIM_OK;
+}
+
+const char* migsim_batch_run_json(migsim_batch_result* r, size_t run) {
+    if (!r || run >= r->n_runs) return nullptr;
+    if (r->json[run].empty()) {
+        const int T = r->T;
+        const size_t v = run / r->seeds.size();
+        const int64_t a0 = r->act_off[run], a1 = r->act_off[run + 1];
+        const int64_t p0 = r->pause_off[run], p1 = r->pause_off[run + 1];
+        mgb::RunResult rr = mgb::assemble(r->spec, r->P, r->variants[v].name, r->seeds[run % r->seeds.size()],
+                                          r->tout.data() + run * T, r->quant.data() + run * T * 4,
+                                          r->actions.data() + a0, static_cast<int>(a1 - a0), r->pauses.data() + p0,
+                                          static_cast<int>(p1 - p0), r->backlog.data() + run * r->R * 2,
+                                          r->rout[run].n_events);
+        r->json[run] = mgb::result_to_json(rr);
+    }
+    return r->json[run].c_str();
+}
+
+int64_t migsim_batch_completions(const migsim_batch_result* r, size_t run, double* out, int64_t cap) {
+    if (!r || run >= r->n_runs || r->comp_off.empty()) return -1;
+    const int64_t c0 = r->comp_off[run], c1 = r->comp_off[run + 1];
+    const int64_t n = c1 - c0;
+    if (out) std::memcpy(out, r->comps.data() + 7 * c0, sizeof(double) * 7 * static_cast<size_t>(std::min(n, cap)));
+    return n;
+}
+
+void migsim_batch_result_free(migsim_batch_result* r) { delete r; }
+
+int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off, size_t n_segments, const double* qs,
+                      size_t n_q, double* out, double* device_ms, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        CK(cudaSetDevice(g->device));
+        const int64_t n = seg_off[n_segments];
+        DevBuf<double> dv, dq, dout;
+        DevBuf<int64_t> doff;
+        dv.alloc(static_cast<size_t>(std::max<int64_t>(n, 1)));
+        dq.alloc(n_q);
+        dout.alloc(n_segments * n_q);
+        doff.alloc(n_segments + 1);
+        cudaStream_t s = g->stream;
+        if (n) CK(cudaMemcpyAsync(dv.p, vals, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(dq.p, qs, sizeof(double) * n_q, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(doff.p, seg_off, sizeof(int64_t) * (n_segments + 1), cudaMemcpyHostToDevice, s));
+        const size_t sm = mg::select_smem_bytes();
+        CK(cudaFuncSetAttribute(mg::select_segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+        CK(cudaEventRecord(g->ev[4], s));
+        mg::select_segments_kernel<<<static_cast<unsigned>(n_segments), 256, sm, s>>>(dv.p, doff.p, static_cast<int>(n_segments),
+                                                                                       dq.p, static_cast<int>(n_q), dout.p);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g->ev[5], s));
+        CK(cudaMemcpyAsync(out, dout.p, sizeof(double) * n_segments * n_q, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, g->ev[4], g->ev[5]));
+        if (device_ms) *device_ms = ms;
+    });
+}
+
+int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, int32_t n_seeds, uint64_t seed_base,
+                    const char* focus_tenant, char** experiment_json, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const auto wall0 = std::chrono::steady_clock::now();
+        if (n_seeds < 1) throw mgb::ConfigError("experiment needs at least one seed");
+        const mgb::ScenarioSpec base = mgb::load_scenario(scenario_path);
+        std::string focus = focus_tenant ? focus_tenant : "";
+        if (focus.empty()) {  // harness.cpp:80-87: smallest tail SLO, first in file order on ties
+            const mgb::TenantEntry* best = nullptr;
+            for (const auto& t : base.tenants)
+                if (!best || t.spec.slo_tail_ms < best->spec.slo_tail_ms) best = &t;
+            focus = best->spec.id;
+        }
+        base.tenant(focus);
+        const std::string p = plan ? plan : "e1";
+        std::vector<mgb::Variant> vs;
+        auto mk = [](const char* name, int en, int mig, int pl, int gu) {
+            mgb::Variant v;
+            v.name = name;
+            v.enabled = en;
+            v.enable_mig = mig;
+            v.enable_placement = pl;
+            v.enable_guardrails = gu;
+            return v;
+        };
+        if (p == "e1" || p == "llm") {
+            vs = {mk("full", 1, 1, 1, 1), mk("static", 0, 0, 0, 0)};
+        } else if (p == "e2") {
+            vs = {mk("full", 1, 1, 1, 1), mk("mig-only", 1, 1, 0, 0), mk("placement-only", 1, 0, 1, 0),
+                  mk("guards-only", 1, 0, 0, 1), mk("static", 0, 0, 0, 0)};
+        } else if (p == "e3") {
+            char name[48];
+            for (double dt : {1.0, 2.0, 5.0}) {
+                std::snprintf(name, sizeof(name), "interval=%.0fs", dt);
+                mgb::Variant v;
+                v.name = name;
+                v.sample_interval_s = dt;
+                vs.push_back(v);
+            }
+            for (int y : {2, 3, 5}) {
+                std::snprintf(name, sizeof(name), "persistence=%d", y);
+                mgb::Variant v;
+                v.name = name;
+                v.persistence_windows = y;
+                vs.push_back(v);
+            }
+            for (int d : {128, 256, 512}) {
+                std::snprintf(name, sizeof(name), "dwell=%d", d);
+                mgb::Variant v;
+                v.name = name;
+                v.dwell_obs = d;
+                v.cooldown_obs = d / 2;
+                vs.push_back(v);
+            }
+        } else {
+            throw mgb::ConfigError("unknown experiment plan '" + p + "'");
+        }
+        std::vector<uint64_t> seeds;
+        for (int s = 0; s < n_seeds; ++s) seeds.push_back(seed_base + static_cast<uint64_t>(s));
+        migsim_batch_result res;
+        run_batch_checked(g, base, vs, seeds, migsim_run_opts{}, res);
+        int fidx = 0;
+        for (int i = 0; i < res.T; ++i)
+            if (res.P.tenant_ids[static_cast<size_t>(i)] == focus) fidx = i;
+        const double window_s = base.duration_s - base.measure_start_s;
+        struct Agg {
+            std::vector<double> p99, miss, thr;
+            double m[3], h[3];
+        };
+        std::vector<Agg> agg(vs.size());
+        for (size_t run = 0; run < res.n_runs; ++run) {
+            Agg& a = agg[run / seeds.size()];
+            const mg::TenantOut& o = res.tout[run * res.T + fidx];
+            const double c = static_cast<double>(o.completed_window);
+            a.p99.push_back(o.completed_window ? res.quant[(run * res.T + fidx) * 4 + 2] : 0.0);
+            a.miss.push_back(o.completed_window ? static_cast<double>(o.window_misses) / c : 0.0);
+            double thr = 0.0;
+            for (int i = 0; i < res.T; ++i) {
+                const mg::TenantOut& x = res.tout[run * res.T + i];
+                thr += x.completed_window ? static_cast<double>(x.completed_window) / window_s : 0.0;
+            }
+            a.thr.push_back(thr);
+        }
+        for (auto& a : agg) {
+            ci(a.p99, a.m[0], a.h[0]);
+            ci(a.miss, a.m[1], a.h[1]);
+            ci(a.thr, a.m[2], a.h[2]);
+        }
+        const Agg* st = nullptr;
+        for (size_t v = 0; v < vs.size(); ++v)
+            if (vs[v].name == "static") st = &agg[v];
+        const double wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+        std::string j = "{\"plan\":" + std::string("\"") + mgb::json_escape(p) + "\",\"scenario\":\"" +
+                        mgb::json_escape(base.name) + "\",\"focus_tenant\":\"" + mgb::json_escape(focus) +
+                        "\",\"wall_s\":" + num(wall_s) + ",\"variants\":[";
+        for (size_t v = 0; v < vs.size(); ++v) {
+            const Agg& a = agg[v];
+            if (v) j += ",";
+            j += "{\"name\":\"" + mgb::json_escape(vs[v].name) + "\",\"seeds\":[";
+            for (size_t s = 0; s < seeds.size(); ++s) j += (s ? "," : "") + std::to_string(seeds[s]);
+            auto arr = [&](const std::vector<double>& x) {
+                std::string o = "[";
+                for (size_t i = 0; i < x.size(); ++i) o += (i ? "," : "") + num(x[i]);
+                return o + "]";
+            };
+            j += "],\"p99_ms\":" + arr(a.p99) + ",\"miss_rate\":" + arr(a.miss) + ",\"throughput_hz\":" + arr(a.thr);
+            const char* names[3] = {"p99_ci", "miss_ci", "throughput_ci"};
+            for (int k = 0; k < 3; ++k)
+                j += ",\"" + std::string(names[k]) + "\":{\"mean\":" + num(a.m[k]) + ",\"half_width\":" + num(a.h[k]) + "}";
+            if (st && vs[v].name != "static" && st->m[0] > 0.0) {
+                j += ",\"p99_delta_pct\":" + num(100.0 * (a.m[0] - st->m[0]) / st->m[0]);
+                if (st->m[1] > 0.0) j += ",\"miss_delta_pct\":" + num(100.0 * (a.m[1] - st->m[1]) / st->m[1]);
+                if (st->m[2] > 0.0) j += ",\"throughput_delta_pct\":" + num(100.0 * (a.m[2] - st->m[2]) / st->m[2]);
+            }
+            j += "}";
+        }
+        j += "]}";
+        char* outp = static_cast<char*>(std::malloc(j.size() + 1));
+        std::memcpy(outp, j.c_str(), j.size() + 1);
+        *experiment_json = outp;
+    });
+}
+
+void migsim_free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,321 @@
+// sm_100a kernels of the batched controller engine (see engine_kernels.cuh for the map to the
+// reference).  Build: nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false -lineinfo
+#include "engine_kernels.cuh"
+
+namespace mg {
+
+// ---------------------------------------------------------------------------------------------
+// arrival-record generation
+__global__ void __launch_bounds__(128) gen_times_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep) {
+    const int T = S->n_tenants;
+    const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= static_cast<int64_t>(n_rep) * T) return;
+    const int t = static_cast<int>(g / n_rep);  // tenant-major: a warp shares one tenant's rate
+    const int r = static_cast<int>(g % n_rep);
+    const PTenant& p = S->tenants[t];
+    uint64_t mt[kMtN];
+    Mt64Ref rng{mt, 0};
+    rng.seed(substream_seed(B.seeds[r], p.name_hash, kArrivals));
+    const int64_t base = static_cast<int64_t>(r) * B.cap_sum + B.off[t];
+    int32_t n_all = 0, n_kept = 0;
+    const bool ok = gen_times(rng, p, S->duration_s, B.t_all + base, B.arr_t + base, B.cap[t], &n_all, &n_kept);
+    B.n_all[r * T + t] = n_all;
+    B.n_kept[r * T + t] = n_kept;
+    if (!ok) atomicExch(B.gen_overflow, 1);
+}
+
+__global__ void __launch_bounds__(128) gen_marks_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep) {
+    const int T = S->n_tenants;
+    const int64_t per = static_cast<int64_t>(n_rep) * T;
+    const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (g >= 4 * per) return;
+    const int purpose = static_cast<int>(g / per);  // purpose-major: warps stay on one code path
+    const int64_t rest = g % per;
+    const int t = static_cast<int>(rest / n_rep);
+    const int r = static_cast<int>(rest % n_rep);
+    const PTenant& p = S->tenants[t];
+    const int64_t base = static_cast<int64_t>(r) * B.cap_sum + B.off[t];
+    uint64_t mt[kMtN];
+    Mt64Ref rng{mt, 0};
+    if (purpose == kMarkIrq) {
+        if (!B.any_irq_noise) return;
+        rng.seed(substream_seed(B.seeds[r], p.name_hash, kIrq));
+        gen_irq(rng, B.n_kept[r * T + t], B.irq_e + base);
+        return;
+    }
+    const uint64_t sp = purpose == kMarkSize ? kTransferSize : purpose == kMarkService ? kService : kNoise;
+    double* out = purpose == kMarkSize ? B.arr_bytes : purpose == kMarkService ? B.arr_mult : B.arr_noise;
+    rng.seed(substream_seed(B.seeds[r], p.name_hash, sp));
+    gen_marks(rng, purpose, p, B.t_all + base, B.n_all[r * T + t], out + base);
+}
+
+// ---------------------------------------------------------------------------------------------
+// replica DES: one warp per replica, working set in dynamic shared memory
+__global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C,
+                                                 WaveBuffers B, int n_rep, SimLayout L) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int r = blockIdx.x;
+    if (r >= n_rep || threadIdx.x != 0) return;
+    const int T = S->n_tenants;
+    const PController& Cv = C[B.variant[r]];
+    SimState& st = *reinterpret_cast<SimState*>(smem);
+    st.td = reinterpret_cast<TenantDyn*>(smem + L.td);
+    st.ctl = reinterpret_cast<TenantCtl*>(smem + L.ctl);
+    st.rd = reinterpret_cast<RootDyn*>(smem + L.rd);
+    Slot* slots = reinterpret_cast<Slot*>(smem + L.slots);
+    double* win;
+    double* vwin;
+    if (B.rings_in_smem) {
+        win = reinterpret_cast<double*>(smem + L.win);
+        vwin = reinterpret_cast<double*>(smem + L.vwin);
+    } else {
+        win = B.rings + static_cast<int64_t>(r) * T * (B.dwell + B.validation);
+        vwin = win + static_cast<int64_t>(T) * B.dwell;
+    }
+    const int64_t base = static_cast<int64_t>(r) * B.cap_sum;
+    ReplicaIO io;
+    io.arr_t = B.arr_t + base;
+    io.arr_bytes = B.arr_bytes + base;
+    io.arr_mult = B.arr_mult + base;
+    io.arr_noise = B.arr_noise + base;
+    io.irq_e = B.irq_e + base;
+    io.off = B.off;
+    io.count = B.n_kept + static_cast<int64_t>(r) * T;
+    io.seed = B.seeds[r];
+    io.req_transfer_ms = B.req_ms + base;
+    io.mt_pause = B.mt_pause + static_cast<int64_t>(r) * T * kMtN;
+    io.win_lat = B.win_lat + base;
+    io.actions = B.actions + static_cast<int64_t>(r) * B.action_cap;
+    io.action_cap = B.action_cap;
+    io.pauses = B.pauses + static_cast<int64_t>(r) * B.pause_cap;
+    io.pause_cap = B.pause_cap;
+    io.tout = B.tout + static_cast<int64_t>(r) * T;
+    io.rout = B.rout + r;
+    io.backlog = B.backlog + static_cast<int64_t>(r) * 2 * S->n_roots;
+    if (B.c_total) {
+        io.c_done = B.c_done + base;
+        io.c_total = B.c_total + base;
+        io.c_compute = B.c_compute + base;
+        io.c_transfer = B.c_transfer + base;
+        io.c_noise = B.c_noise + base;
+    } else {
+        io.c_done = io.c_total = io.c_compute = io.c_transfer = io.c_noise = nullptr;
+    }
+    Sim<HostLanes> sim(*S, Cv, io, st, slots, HostLanes{});
+    sim.init(B.file_order, win, vwin);
+    sim.run();
+    sim.finish();
+}
+
+// ---------------------------------------------------------------------------------------------
+// nearest-rank select (engine.cpp:800-816; rank = max(1, ceil(q n)), value at rank-1 of the sort)
+namespace {
+
+constexpr int kSelThreads = 256;
+constexpr int kDigitBits = 11;
+constexpr int kBins = 1 << kDigitBits;
+constexpr int kMaxQ = 4;
+constexpr int kGather = 1024;
+
+__device__ __forceinline__ uint64_t order_key(double x) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+struct SelectSmem {
+    uint32_t hist[kMaxQ][kBins];
+    uint64_t cand[kMaxQ][kGather];
+    uint32_t part[kSelThreads];
+    uint64_t prefix[kMaxQ];
+    int64_t kk[kMaxQ];
+    int64_t gsize[kMaxQ];
+    int32_t shift[kMaxQ];
+    int32_t owner[kMaxQ];  // quantile whose histogram this one shares (identical group)
+    uint32_t cnt[kMaxQ];
+    int32_t done[kMaxQ];
+    double result[kMaxQ];
+    int32_t gather;
+};
+
+__device__ __forceinline__ bool in_group(uint64_t key, uint64_t prefix, int shift) {
+    return shift >= 64 ? true : ((key ^ prefix) >> shift) == 0;
+}
+
+// One CTA selects ranks of nq quantiles over vals[0..n).
+__device__ void block_select(const double* __restrict__ vals, int64_t n, const double* qs, int nq, double* out,
+                             SelectSmem& sm) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    if (n <= 0) {
+        if (tid < nq) out[tid] = 0.0;
+        return;
+    }
+    if (tid < nq) {
+        int64_t rank = static_cast<int64_t>(ceil(__dmul_rn(qs[tid], static_cast<double>(n))));
+        if (rank < 1) rank = 1;
+        if (rank > n) rank = n;
+        sm.kk[tid] = rank - 1;
+        sm.prefix[tid] = 0;
+        sm.shift[tid] = 64;
+        sm.gsize[tid] = n;
+        sm.done[tid] = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        // which quantiles still need a histogram pass; share identical groups
+        if (tid == 0) {
+            bool small = true;
+            for (int q = 0; q < nq; ++q) {
+                sm.owner[q] = q;
+                if (sm.done[q]) continue;
+                if (sm.shift[q] == 0 || sm.gsize[q] == 1) continue;
+                if (sm.gsize[q] > kGather) small = false;
+                for (int p = 0; p < q; ++p)
+                    if (!sm.done[p] && sm.prefix[p] == sm.prefix[q] && sm.shift[p] == sm.shift[q]) {
+                        sm.owner[q] = p;
+                        break;
+                    }
+            }
+            sm.gather = small;
+        }
+        __syncthreads();
+        if (sm.gather) break;
+        for (int q = 0; q < nq; ++q)
+            for (int b = tid; b < kBins; b += kSelThreads) sm.hist[q][b] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += kSelThreads) {
+            const uint64_t key = order_key(vals[i]);
+            for (int q = 0; q < nq; ++q) {
+                const int sh = sm.shift[q];
+                const bool active = !sm.done[q] && sm.owner[q] == q && sm.shift[q] > 0 && in_group(key, sm.prefix[q], sh);
+                const int d = sh < kDigitBits ? sh : kDigitBits;
+                const uint32_t digit = active ? static_cast<uint32_t>((key >> (sh - d)) & ((1u << d) - 1)) : 0xffffffffu;
+                // warp-aggregated histogram increments (skewed digits would serialize smem atomics)
+                const unsigned peers = __match_any_sync(__activemask(), digit);
+                if (active && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[q][digit], __popc(peers));
+            }
+        }
+        __syncthreads();
+        // locate each quantile's digit: per-thread partial sums of 8 bins, block scan
+        for (int q = 0; q < nq; ++q) {
+            if (sm.done[q] || sm.shift[q] == 0 || sm.gsize[q] == 1) continue;
+            const int o = sm.owner[q];
+            constexpr int per = kBins / kSelThreads;
+            uint32_t s = 0;
+            for (int b = 0; b < per; ++b) s += sm.hist[o][tid * per + b];
+            sm.part[tid] = s;
+            __syncthreads();
+            if (tid == 0) {
+                int64_t acc = 0;
+                int th = 0;
+                while (th < kSelThreads - 1 && acc + sm.part[th] <= sm.kk[q]) acc += sm.part[th++];
+                int bin = th * per;
+                while (acc + sm.hist[o][bin] <= sm.kk[q]) acc += sm.hist[o][bin++];
+                const int sh = sm.shift[q];
+                const int d = sh < kDigitBits ? sh : kDigitBits;
+                sm.prefix[q] |= static_cast<uint64_t>(bin) << (sh - d);
+                sm.shift[q] = sh - d;
+                sm.kk[q] -= acc;
+                sm.gsize[q] = sm.hist[o][bin];
+            }
+            __syncthreads();
+        }
+    }
+    // resolve: fully determined groups directly, the rest by gathering the (small) group
+    if (tid < nq) sm.cnt[tid] = 0;
+    __syncthreads();
+    bool need_gather = false;
+    for (int q = 0; q < nq; ++q) need_gather |= !(sm.shift[q] == 0 || sm.gsize[q] == 1);
+    if (need_gather) {
+        for (int64_t i = tid; i < n; i += kSelThreads) {
+            const uint64_t key = order_key(vals[i]);
+            for (int q = 0; q < nq; ++q) {
+                if (sm.shift[q] == 0 || sm.gsize[q] == 1) continue;
+                if (in_group(key, sm.prefix[q], sm.shift[q])) {
+                    const uint32_t k = atomicAdd(&sm.cnt[q], 1u);
+                    if (k < kGather) sm.cand[q][k] = key;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    for (int q = 0; q < nq; ++q) {
+        if (sm.shift[q] == 0) {
+            if (tid == 0) sm.result[q] = key_value(sm.prefix[q]);
+        } else if (sm.gsize[q] == 1) {
+            // the single group member: find it
+            if (tid == 0) sm.result[q] = 0.0;
+            __syncthreads();
+            for (int64_t i = tid; i < n; i += kSelThreads) {
+                const uint64_t key = order_key(vals[i]);
+                if (in_group(key, sm.prefix[q], sm.shift[q])) sm.result[q] = key_value(key);
+            }
+        } else {
+            const int m = static_cast<int>(sm.gsize[q]);
+            for (int a = tid; a < m; a += kSelThreads) {
+                const uint64_t v = sm.cand[q][a];
+                int lt = 0, le = 0;
+                for (int b = 0; b < m; ++b) {
+                    lt += sm.cand[q][b] < v;
+                    le += sm.cand[q][b] <= v;
+                }
+                if (lt <= sm.kk[q] && sm.kk[q] < le) sm.result[q] = key_value(v);
+            }
+        }
+        __syncthreads();
+    }
+    if (tid < nq) out[tid] = sm.result[tid];
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kSelThreads) select_kernel(WaveBuffers B, int T, int n_rep) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SelectSmem& sm = *reinterpret_cast<SelectSmem*>(smem);
+    const int s = blockIdx.x;
+    if (s >= n_rep * T) return;
+    const int r = s / T, t = s % T;
+    const int64_t n = static_cast<int64_t>(B.tout[s].completed_window);
+    const double qs[kMaxQ] = {0.50, 0.95, 0.99, 0.999};
+    block_select(B.win_lat + static_cast<int64_t>(r) * B.cap_sum + B.off[t], n, qs, kMaxQ, B.quant + 4ll * s, sm);
+}
+
+__global__ void __launch_bounds__(kSelThreads) select_segments_kernel(const double* __restrict__ vals,
+                                                                      const int64_t* __restrict__ seg_off, int n_seg,
+                                                                      const double* __restrict__ qs, int nq,
+                                                                      double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    SelectSmem& sm = *reinterpret_cast<SelectSmem*>(smem);
+    const int s = blockIdx.x;
+    if (s >= n_seg) return;
+    for (int q0 = 0; q0 < nq; q0 += kMaxQ) {
+        const int cnt = nq - q0 < kMaxQ ? nq - q0 : kMaxQ;
+        block_select(vals + seg_off[s], seg_off[s + 1] - seg_off[s], qs + q0, cnt, out + static_cast<int64_t>(s) * nq + q0, sm);
+        __syncthreads();
+    }
+}
+
+size_t select_smem_bytes() { return sizeof(SelectSmem); }
+
+// ---------------------------------------------------------------------------------------------
+__global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
+                                       const int64_t* __restrict__ dst_off, ActionRec* __restrict__ dst, int n_rep) {
+    const int r = blockIdx.x;
+    if (r >= n_rep) return;
+    const int n = rout[r].n_actions < cap ? rout[r].n_actions : cap;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) dst[dst_off[r] + k] = src[static_cast<int64_t>(r) * cap + k];
+}
+
+__global__ void compact_pauses_kernel(const PauseRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
+                                      const int64_t* __restrict__ dst_off, PauseRec* __restrict__ dst, int n_rep) {
+    const int r = blockIdx.x;
+    if (r >= n_rep) return;
+    const int n = rout[r].n_pauses < cap ? rout[r].n_pauses : cap;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) dst[dst_off[r] + k] = src[static_cast<int64_t>(r) * cap + k];
+}
+
+}  // namespace mg

@@ -1,0 +1,60 @@
+// sm_100a kernels of the batched controller engine.
+//
+//  gen_times_kernel   one thread per (replica, tenant): arrival clock stream (gamma renewal) +
+//                     schedule thinning                         (workload.cpp:129-136, engine.cpp:435-446)
+//  gen_marks_kernel   one thread per (replica, tenant, stream): transfer-size / service / noise
+//                     marks and the IRQ exponential stream      (workload.cpp:138-156, engine.cpp:403-404)
+//  des_kernel         one warp per replica, state in shared memory: the event loop + controller
+//                     (engine.cpp:864-894, controller.cpp:489-603)
+//  select_kernel      one CTA per (replica, tenant): nearest-rank p50/p95/p99/p999 of the measurement
+//                     window by an 11-bit MSD radix select over the order-preserving bit image of the
+//                     FP64 latencies                            (engine.cpp:800-816)
+//  compact_kernel     gathers the variable-length action / pause logs into dense host-bound buffers
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "../common/des_core.h"
+
+namespace mg {
+
+struct WaveBuffers {
+    // [W][cap_sum] arrays
+    double *arr_t, *arr_bytes, *arr_mult, *arr_noise, *irq_e, *t_all, *req_ms, *win_lat;
+    double *c_done, *c_total, *c_compute, *c_transfer, *c_noise;  // optional
+    int32_t *n_all, *n_kept;                                       // [W][T]
+    uint64_t* mt_pause;                                            // [W][T][312]
+    ActionRec* actions;                                            // [W][action_cap]
+    PauseRec* pauses;                                              // [W][pause_cap]
+    TenantOut* tout;                                               // [W][T]
+    ReplicaOut* rout;                                              // [W]
+    double* backlog;                                               // [W][R][2]
+    double* quant;                                                 // [W][T][4]
+    double* rings;                                                 // [W][T][dwell + validation] when not in smem
+    const uint64_t* seeds;                                         // [W]
+    const int32_t* variant;                                        // [W]
+    const int64_t* off;                                            // [T]
+    const int64_t* cap;                                            // [T]
+    const int32_t* file_order;                                     // [T]
+    int32_t* gen_overflow;                                         // [1]
+    int64_t cap_sum;
+    int32_t action_cap, pause_cap;
+    int32_t any_irq_noise, rings_in_smem;
+    int32_t dwell, validation;  // ring strides (max over variants)
+};
+
+__global__ void gen_times_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep);
+__global__ void gen_marks_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep);
+__global__ void des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
+                           int n_rep, SimLayout L);
+__global__ void select_kernel(WaveBuffers B, int T, int n_rep);
+__global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
+                                       const int64_t* __restrict__ dst_off, ActionRec* __restrict__ dst, int n_rep);
+__global__ void compact_pauses_kernel(const PauseRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
+                                      const int64_t* __restrict__ dst_off, PauseRec* __restrict__ dst, int n_rep);
+
+// standalone nearest-rank select over arbitrary segments (C-ABI migsim_gpu_select)
+__global__ void select_segments_kernel(const double* __restrict__ vals, const int64_t* __restrict__ seg_off,
+                                       int n_seg, const double* __restrict__ qs, int nq, double* __restrict__ out);
+
+}  // namespace mg

@@ -113,6 +113,18 @@ MIGSIM_API int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scen
                     const char* focus_tenant, char** experiment_json, char* err, size_t errlen);
 MIGSIM_API void migsim_free(void* p);
 
+/* ---- diagnostics used by the parity tests ---------------------------------------------- */
+/* Host-only: parse a scenario (path) with the engine's scenario-v1 loader and return the
+ * normalised spec as JSON (no GPU needed). */
+MIGSIM_API int migsim_scenario_dump(const char* path, char** json, char* err, size_t errlen);
+/* Device glibc-exact math: fn 0 = log(x), 1 = exp(x), 2 = pow(x, y); n values. */
+MIGSIM_API int migsim_gpu_libm(migsim_gpu* g, int fn, const double* x, const double* y, double* out, size_t n,
+                               char* err, size_t errlen);
+/* Device-generated arrival records of one tenant (canonical index) for one seed:
+ * 4 doubles per kept arrival {t_s, transfer_bytes, service_mult, noise_ms}; *n_out = count. */
+MIGSIM_API int migsim_gpu_arrivals(migsim_gpu* g, int32_t scenario_id, uint64_t seed, int32_t tenant, double* out,
+                                   int64_t cap, int64_t* n_out, char* err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -707,4 +707,180 @@ int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, 
 
 void migsim_free(void* p) { std::free(p); }
 
+int migsim_scenario_dump(const char* path, char** json, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const mgb::ScenarioSpec s = mgb::load_scenario(path);
+        auto sched = [](const mgb::InterferenceSchedule& x) {
+            std::string o = "{\"kind\":\"";
+            o += x.kind == mgb::InterferenceSchedule::Kind::always ? "always"
+                 : x.kind == mgb::InterferenceSchedule::Kind::square_wave ? "square_wave" : "phases";
+            o += "\",\"period_s\":" + num(x.period_s) + ",\"duty\":" + num(x.duty) + ",\"offset_s\":" + num(x.offset_s) +
+                 ",\"phases\":[";
+            for (size_t i = 0; i < x.phases.size(); ++i)
+                o += (i ? "," : "") + std::string("[") + num(x.phases[i].start_s) + "," + num(x.phases[i].end_s) + "]";
+            return o + "]}";
+        };
+        std::string j = "{\"name\":\"" + mgb::json_escape(s.name) + "\",\"duration_s\":" + num(s.duration_s) +
+                        ",\"measure_start_s\":" + num(s.measure_start_s) +
+                        ",\"fabric_redistribute\":" + (s.fabric_redistribute ? "true" : "false") + ",\"hosts\":[";
+        for (size_t h = 0; h < s.topology.hosts.size(); ++h) {
+            const auto& H = s.topology.hosts[h];
+            j += (h ? "," : "") + std::string("{\"numa_domains\":") + std::to_string(H.numa_domains) +
+                 ",\"io_capacity_Bps\":" + num(H.io_capacity_Bps) + ",\"irq_hot_core_groups\":[";
+            size_t k = 0;
+            for (int c : H.irq_hot_core_groups) j += (k++ ? "," : "") + std::to_string(c);
+            j += "],\"pcie_roots\":[";
+            for (size_t r = 0; r < H.pcie_roots.size(); ++r)
+                j += (r ? "," : "") + std::string("{\"id\":") + std::to_string(H.pcie_roots[r].id) +
+                     ",\"capacity_Bps\":" + num(H.pcie_roots[r].capacity_Bps) + "}";
+            j += "],\"gpus\":[";
+            for (size_t g2 = 0; g2 < H.gpus.size(); ++g2) {
+                const auto& G = H.gpus[g2];
+                j += (g2 ? "," : "") + std::string("{\"id\":") + std::to_string(G.id) + ",\"pcie_root_id\":" +
+                     std::to_string(G.pcie_root_id) + ",\"numa_id\":" + std::to_string(G.numa_id) + ",\"core_group\":" +
+                     std::to_string(G.core_group) + ",\"total_slices\":" + std::to_string(G.total_slices) +
+                     ",\"mig_enabled\":" + (G.mig_enabled ? "true" : "false") + "}";
+            }
+            j += "]}";
+        }
+        j += "],\"tenants\":[";
+        for (size_t i = 0; i < s.tenants.size(); ++i) {
+            const auto& e = s.tenants[i];
+            const auto& t = e.spec;
+            j += (i ? "," : "") + std::string("{\"id\":\"") + mgb::json_escape(t.id) + "\",\"class\":\"" +
+                 mgb::to_string(t.tclass) + "\",\"arrival_rate_hz\":" + num(t.arrival_rate_hz) + ",\"arrival_cv\":" +
+                 num(t.arrival_cv) + ",\"transfer_mix\":[";
+            for (size_t m = 0; m < t.transfer_mix.size(); ++m)
+                j += (m ? "," : "") + std::string("[") + num(t.transfer_mix[m].bytes) + "," + num(t.transfer_mix[m].weight) + "]";
+            j += "],\"base_compute_ms\":" + num(t.base_compute_ms) + ",\"service_cv\":" + num(t.service_cv) +
+                 ",\"slo_tail_ms\":" + num(t.slo_tail_ms) + ",\"weight\":" + num(t.weight) + ",\"pcie_cap_Bps\":" +
+                 num(t.pcie_cap_Bps) + ",\"host_io_Bps\":" + num(t.host_io_Bps) + ",\"sm_demand\":" + num(t.sm_demand) +
+                 ",\"noise_mean_ms\":" + num(t.noise_mean_ms) + ",\"host\":" + std::to_string(e.placement.host) +
+                 ",\"gpu\":" + std::to_string(e.placement.gpu) + ",\"first_slice\":" +
+                 std::to_string(e.placement.slices.first) + ",\"slice_count\":" + std::to_string(e.placement.slices.count) +
+                 ",\"profile\":\"" + e.profile_name + "\",\"schedule\":" + sched(e.schedule) + "}";
+        }
+        j += "],\"irq_bursts\":[";
+        for (size_t b = 0; b < s.irq_bursts.size(); ++b) {
+            const auto& q = s.irq_bursts[b];
+            j += (b ? "," : "") + std::string("{\"host\":") + std::to_string(q.host) + ",\"core_group\":" +
+                 std::to_string(q.core_group) + ",\"extra_noise_ms\":" + num(q.extra_noise_ms) + ",\"schedule\":" +
+                 sched(q.schedule) + "}";
+        }
+        const auto& c = s.controller;
+        auto B = [](bool v) { return std::string(v ? "true" : "false"); };
+        j += "],\"controller\":{\"enabled\":" + B(c.enabled) + ",\"enable_mig\":" + B(c.enable_mig) +
+             ",\"enable_placement\":" + B(c.enable_placement) + ",\"enable_guardrails\":" + B(c.enable_guardrails) +
+             ",\"tail_threshold_ms\":" + num(c.tail_threshold_ms) + ",\"persistence_windows\":" +
+             std::to_string(c.persistence_windows) + ",\"dwell_obs\":" + std::to_string(c.dwell_obs) +
+             ",\"cooldown_obs\":" + std::to_string(c.cooldown_obs) + ",\"sample_interval_s\":" + num(c.sample_interval_s) +
+             ",\"warmup_s\":" + num(c.warmup_s) + ",\"move_futility_ratio\":" + num(c.move_futility_ratio) +
+             ",\"throttle_duration_s\":" + num(c.throttle_duration_s) + ",\"quota_duration_s\":" +
+             num(c.quota_duration_s) + ",\"ema_alpha\":" + num(c.ema_alpha) + ",\"hysteresis_clear_ratio\":" +
+             num(c.hysteresis_clear_ratio) + ",\"relax_stability_ratio\":" + num(c.relax_stability_ratio) +
+             ",\"relax_score_threshold\":" + num(c.relax_score_threshold) + ",\"validation_obs\":" +
+             std::to_string(c.validation_obs) + ",\"rollback_regress_ratio\":" + num(c.rollback_regress_ratio) +
+             ",\"diag_pcie_util_threshold\":" + num(c.diag_pcie_util_threshold) + ",\"diag_host_io_threshold\":" +
+             num(c.diag_host_io_threshold) + ",\"diag_sm_util_threshold\":" + num(c.diag_sm_util_threshold) +
+             ",\"move_margin\":" + num(c.move_margin) + ",\"admission_queue_timeout_epochs\":" +
+             std::to_string(c.admission_queue_timeout_epochs) + ",\"guardrail_io_throttle_Bps\":" +
+             num(c.guardrail_io_throttle_Bps) + ",\"guardrail_mps_quota_pct\":" + num(c.guardrail_mps_quota_pct) +
+             ",\"irq_lookback_s\":" + num(c.irq_lookback_s) + ",\"throughput_floor\":" + num(c.throughput_floor) + "}}";
+        char* o = static_cast<char*>(std::malloc(j.size() + 1));
+        std::memcpy(o, j.c_str(), j.size() + 1);
+        *json = o;
+    });
+}
+
+int migsim_gpu_libm(migsim_gpu* g, int fn, const double* x, const double* y, double* out, size_t n, char* err,
+                    size_t errlen) {
+    return guarded(err, errlen, [&] {
+        CK(cudaSetDevice(g->device));
+        DevBuf<double> dx, dy, dout;
+        dx.alloc(n);
+        dy.alloc(n);
+        dout.alloc(n);
+        cudaStream_t s = g->stream;
+        CK(cudaMemcpyAsync(dx.p, x, 8 * n, cudaMemcpyHostToDevice, s));
+        if (y) CK(cudaMemcpyAsync(dy.p, y, 8 * n, cudaMemcpyHostToDevice, s));
+        else CK(cudaMemsetAsync(dy.p, 0, 8 * n, s));
+        mg::libm_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(fn, dx.p, dy.p, dout.p,
+                                                                               static_cast<int64_t>(n));
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(out, dout.p, 8 * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+int migsim_gpu_arrivals(migsim_gpu* g, int32_t scenario_id, uint64_t seed, int32_t tenant, double* out, int64_t cap,
+                        int64_t* n_out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
+            throw mgb::ConfigError("unknown scenario id");
+        CK(cudaSetDevice(g->device));
+        const mgb::Packed P = mgb::pack(g->scenarios[static_cast<size_t>(scenario_id)], {});
+        const int T = P.scen.n_tenants;
+        if (tenant < 0 || tenant >= T) throw mgb::ConfigError("tenant index out of range");
+        WaveAlloc A;
+        const size_t big = static_cast<size_t>(P.cap_sum);
+        A.arr_t.alloc(big);
+        A.arr_bytes.alloc(big);
+        A.arr_mult.alloc(big);
+        A.arr_noise.alloc(big);
+        A.irq_e.alloc(big);
+        A.t_all.alloc(big);
+        A.n_all.alloc(T);
+        A.n_kept.alloc(T);
+        A.seeds.alloc(1);
+        A.gen_overflow.alloc(1);
+        A.off.alloc(T);
+        A.cap.alloc(T);
+        A.scen.alloc(1);
+        cudaStream_t s = g->stream;
+        CK(cudaMemcpyAsync(A.scen.p, &P.scen, sizeof(mg::PScenario), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(A.off.p, P.off.data(), 8 * T, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(A.cap.p, P.cap.data(), 8 * T, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(A.seeds.p, &seed, 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(A.gen_overflow.p, 0, 4, s));
+        mg::WaveBuffers B{};
+        B.arr_t = A.arr_t.p;
+        B.arr_bytes = A.arr_bytes.p;
+        B.arr_mult = A.arr_mult.p;
+        B.arr_noise = A.arr_noise.p;
+        B.irq_e = A.irq_e.p;
+        B.t_all = A.t_all.p;
+        B.n_all = A.n_all.p;
+        B.n_kept = A.n_kept.p;
+        B.seeds = A.seeds.p;
+        B.off = A.off.p;
+        B.cap = A.cap.p;
+        B.gen_overflow = A.gen_overflow.p;
+        B.cap_sum = P.cap_sum;
+        B.any_irq_noise = P.any_irq_noise;
+        mg::gen_times_kernel<<<static_cast<unsigned>((T + 127) / 128), 128, 0, s>>>(A.scen.p, B, 1);
+        mg::gen_marks_kernel<<<static_cast<unsigned>((4 * T + 127) / 128), 128, 0, s>>>(A.scen.p, B, 1);
+        CK(cudaGetLastError());
+        std::vector<int32_t> nk(T);
+        CK(cudaMemcpyAsync(nk.data(), A.n_kept.p, 4 * T, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t n = nk[tenant];
+        *n_out = n;
+        const int64_t m = std::min(n, cap);
+        std::vector<double> a(static_cast<size_t>(std::max<int64_t>(m, 1))), b(a), c(a), d(a);
+        const int64_t o = P.off[tenant];
+        if (m > 0) {
+            CK(cudaMemcpy(a.data(), A.arr_t.p + o, 8 * m, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(b.data(), A.arr_bytes.p + o, 8 * m, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(c.data(), A.arr_mult.p + o, 8 * m, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(d.data(), A.arr_noise.p + o, 8 * m, cudaMemcpyDeviceToHost));
+        }
+        for (int64_t k = 0; k < m; ++k) {
+            out[4 * k + 0] = a[k];
+            out[4 * k + 1] = b[k];
+            out[4 * k + 2] = c[k];
+            out[4 * k + 3] = d[k];
+        }
+    });
+}
+
 }  // extern "C"

@@ -319,3 +319,12 @@ __global__ void compact_pauses_kernel(const PauseRec* __restrict__ src, int cap,
 }
 
 }  // namespace mg
+
+namespace mg {
+__global__ void libm_kernel(int fn, const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ out,
+                            int64_t n) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    out[i] = fn == 0 ? gl_log(x[i]) : fn == 1 ? gl_exp(x[i]) : gl_pow(x[i], y[i]);
+}
+}  // namespace mg

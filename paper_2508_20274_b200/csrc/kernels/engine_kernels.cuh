@@ -58,3 +58,8 @@ __global__ void select_segments_kernel(const double* __restrict__ vals, const in
                                        int n_seg, const double* __restrict__ qs, int nq, double* __restrict__ out);
 
 }  // namespace mg
+
+namespace mg {
+__global__ void libm_kernel(int fn, const double* __restrict__ x, const double* __restrict__ y, double* __restrict__ out,
+                            int64_t n);
+}

@@ -1,0 +1,159 @@
+"""CPU tests of the engine's own logic (no GPU): glibc-exact math, the arrival generator, the
+scenario loader, and the full replica simulator (compiled for the CPU as a test harness) against
+the compiled reference."""
+import ctypes
+import json
+import os
+
+import numpy as np
+import pytest
+
+from tests._libs import (CONFIG_SCENARIOS, GOLDEN_SCENARIOS, PRODUCT_SO, build_product, diff_results, hostsim,
+                         hostsim_run, oracle, ref_run, scenario_json)
+
+LIBM = ctypes.CDLL("libm.so.6")
+for _f in ("log", "exp"):
+    getattr(LIBM, _f).restype = ctypes.c_double
+    getattr(LIBM, _f).argtypes = [ctypes.c_double]
+LIBM.pow.restype = ctypes.c_double
+LIBM.pow.argtypes = [ctypes.c_double, ctypes.c_double]
+
+
+def _math_inputs(n, rng):
+    bits = rng.integers(0, 2**63, n, dtype=np.int64).astype(np.uint64) | (rng.integers(0, 2, n).astype(np.uint64) << 63)
+    anyv = bits.view(np.float64)
+    unit = rng.random(n)
+    near1 = 1.0 + (rng.random(n) - 0.5) * 0.25
+    wide = (rng.random(n) - 0.5) * 1400
+    return np.concatenate([anyv, unit, near1, wide, [0.0, -0.0, 1.0, np.inf, -np.inf, np.nan, 5e-324, 1e-310]])
+
+
+@pytest.mark.parametrize("fn", [0, 1, 2])
+def test_glibc_math_bit_exact(fn):
+    """glibc_math.h vs the host's libm (the FMA IFUNC variants the reference links)."""
+    rng = np.random.default_rng(100 + fn)
+    x = np.ascontiguousarray(_math_inputs(60000, rng))
+    if fn == 2:
+        x = np.abs(x)
+        y = np.ascontiguousarray(np.concatenate([rng.uniform(0.5, 3.0, len(x) - 8), [0.5, 2.0, -1.5, 1e-70, 1e300,
+                                                                                    np.nan, 0.0, -0.0]]))
+    else:
+        y = np.zeros_like(x)
+    out = np.zeros_like(x)
+    hostsim().hostsim_math(fn, x.ctypes.data, y.ctypes.data, out.ctypes.data, len(x))
+    f = [LIBM.log, LIBM.exp, None][fn]
+    ref = np.array([LIBM.pow(a, b) for a, b in zip(x, y)] if fn == 2 else [f(a) for a in x])
+    same = (out.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(out) & np.isnan(ref))
+    assert same.all(), (x[~same][:5], out[~same][:5], ref[~same][:5])
+
+
+@pytest.mark.parametrize("path", GOLDEN_SCENARIOS + CONFIG_SCENARIOS)
+def test_arrival_streams_bit_exact(path):
+    """generator (gen_times/gen_marks of arrivals.h) vs workload::generate_arrivals."""
+    spec = json.loads(ctypes.string_at(oracle().ref_scenario_dump(scenario_json(path), b"x")).decode())
+    ids = sorted(t["id"] for t in spec["tenants"])
+    sj = scenario_json(path)
+    for seed in (1, 17):
+        for ti, tid in enumerate(ids):
+            cap = 2_000_000
+            ref = np.zeros((cap, 4))
+            n = oracle().ref_generate_arrivals(sj, tid.encode(), seed, spec["duration_s"], ref.ctypes.data, cap)
+            mine = np.zeros((cap, 4))
+            m = hostsim().hostsim_arrivals(path.encode(), seed, ti, mine.ctypes.data, cap)
+            assert n == m
+            assert (ref[:n].view(np.uint64) == mine[:m].view(np.uint64)).all()
+
+
+def _product():
+    if not os.path.exists(PRODUCT_SO):
+        build_product()
+    lib = ctypes.CDLL(PRODUCT_SO)
+    lib.migsim_scenario_dump.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p,
+                                         ctypes.c_size_t]
+    lib.migsim_free.argtypes = [ctypes.c_void_p]
+    return lib
+
+
+def _dump(path):
+    lib = _product()
+    out = ctypes.c_void_p()
+    err = ctypes.create_string_buffer(1024)
+    rc = lib.migsim_scenario_dump(path.encode(), ctypes.byref(out), err, 1024)
+    if rc != 0:
+        return rc, err.value.decode()
+    s = ctypes.string_at(out.value).decode()
+    lib.migsim_free(out)
+    return 0, json.loads(s)
+
+
+@pytest.mark.parametrize("path", GOLDEN_SCENARIOS + CONFIG_SCENARIOS)
+def test_scenario_loader_matches_reference(path):
+    rc, mine = _dump(path)
+    assert rc == 0, mine
+    p = oracle().ref_scenario_dump(scenario_json(path), path.encode())
+    ref = json.loads(ctypes.string_at(p).decode())
+    oracle().ref_free(p)
+    assert mine == ref
+
+
+@pytest.mark.parametrize("mutation,expect", [
+    (("version: scenario-v1", "version: scenario-v2"), ":7: unsupported scenario version 'scenario-v2'"),
+    (("    arrival_rate_hz: 65", "    arrival_rate_hz: 65\n    arival_cv: 1.0"), ":31: unknown key 'arival_cv' in tenant"),
+    (("duration_s: 1800", "duration_s: soon"), ":9: value of 'duration_s' is not a number"),
+    (("profile: 2g.20gb, first_slice: 0 }", "profile: 9g.90gb, first_slice: 0 }"), "unknown MIG profile '9g.90gb'"),
+    (("first_slice: 6 }", "first_slice: 1 }"), "overlap on GPU 0"),
+    (("kind: square_wave, period_s: 120", "kind: sine, period_s: 120"), "unknown schedule kind 'sine'"),
+])
+def test_scenario_loader_errors(tmp_path, mutation, expect):
+    """scenario.cpp error semantics: allowlists, version gate, typed values, cross-checks, file:line."""
+    src = open(GOLDEN_SCENARIOS[0]).read()
+    assert mutation[0] in src
+    p = tmp_path / "bad.yaml"
+    p.write_text(src.replace(mutation[0], mutation[1], 1))
+    rc, msg = _dump(str(p))
+    assert rc == 1 and expect in msg, msg
+
+
+def test_yaml_numbers_follow_yaml_cpp(tmp_path):
+    """12e9 is a double for yaml-cpp (YAML 1.1 would say string)."""
+    rc, spec = _dump(GOLDEN_SCENARIOS[0])
+    assert spec["hosts"][0]["pcie_roots"][0]["capacity_Bps"] == 12e9
+
+
+FAST_CASES = [(GOLDEN_SCENARIOS[1], s) for s in (1, 2, 3)] + [(GOLDEN_SCENARIOS[0], 1), (GOLDEN_SCENARIOS[3], 1),
+                                                              (CONFIG_SCENARIOS[2], 1), (CONFIG_SCENARIOS[0], 2)]
+VARIANTS = [None, dict(enabled=True, enable_mig=True, enable_placement=False, enable_guardrails=False),
+            dict(enabled=True, enable_mig=False, enable_placement=True, enable_guardrails=False),
+            dict(enabled=True, enable_mig=False, enable_placement=False, enable_guardrails=True),
+            dict(enabled=False, enable_mig=False, enable_placement=False, enable_guardrails=False)]
+
+
+@pytest.mark.parametrize("path,seed", FAST_CASES)
+@pytest.mark.parametrize("vi", range(len(VARIANTS)))
+def test_replica_logic_vs_reference(path, seed, vi):
+    """The replica simulator + controller (des_core.h) compiled for the CPU vs engine::run_scenario."""
+    v = VARIANTS[vi]
+    ref, _ = ref_run(path, seed, v)
+    mine = hostsim_run(path, seed, v)
+    assert diff_results(ref, mine) == []
+
+
+def test_replica_logic_large_scenarios():
+    for path, seed in ((CONFIG_SCENARIOS[1], 1), (GOLDEN_SCENARIOS[2], 1)):
+        ref, _ = ref_run(path, seed)
+        assert diff_results(ref, hostsim_run(path, seed)) == []
+
+
+def test_capi_exports_every_declared_symbol():
+    """The C-ABI library loads and exports every entry point include/migsim_b200.h declares."""
+    import re
+
+    hdr = open(os.path.join(os.path.dirname(PRODUCT_SO), "..", "..", "include", "migsim_b200.h")).read()
+    declared = set(re.findall(r"MIGSIM_API\s+[\w\s\*]+?\b(migsim_\w+)\s*\(", hdr))
+    assert len(declared) >= 20
+    lib = _product()
+    for name in declared:
+        assert hasattr(lib, name), name
+    from paper_2508_20274_b200.api import EXPORTED_SYMBOLS
+
+    assert set(EXPORTED_SYMBOLS) <= declared

@@ -1,0 +1,122 @@
+"""GPU parity: the sm_100a engine through its C-ABI vs the compiled reference, bit-exact.
+
+Outputs compared (north_star bar): action sequences (kind, tenant, target, t_s, placement detail,
+p99/EMA at decision, breach windows, obs counters, pauses, rollbacks), percentile values (nearest
+rank -> indices bit-exact), SLO-miss and completion counts, end states, stability flags and notes.
+FP64 values are required bit-identical (stricter than the 1e-9 relative the spec allows).
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import restate
+from tests._libs import CONFIG_SCENARIOS, GOLDEN_SCENARIOS, diff_results, oracle, ref_run, scenario_json
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = [
+    ("full", dict(enabled=True, enable_mig=True, enable_placement=True, enable_guardrails=True)),
+    ("mig-only", dict(enabled=True, enable_mig=True, enable_placement=False, enable_guardrails=False)),
+    ("placement-only", dict(enabled=True, enable_mig=False, enable_placement=True, enable_guardrails=False)),
+    ("guards-only", dict(enabled=True, enable_mig=False, enable_placement=False, enable_guardrails=True)),
+    ("static", dict(enabled=False, enable_mig=False, enable_placement=False, enable_guardrails=False)),
+]
+
+
+def _variants():
+    from paper_2508_20274_b200 import Variant
+
+    return [Variant(n, **v) for n, v in VARIANTS]
+
+
+@pytest.mark.parametrize("path", GOLDEN_SCENARIOS + CONFIG_SCENARIOS)
+def test_scenarios_all_variants(engine, path):
+    """Every shipped scenario + C1..C3, 5-variant ablation grid x 3 seeds in ONE batched call."""
+    fast = "stability" not in path and "c2" not in path
+    seeds = [1, 2, 3] if fast else [1]
+    sid = engine.load_scenario(path)
+    res = engine.run_batch(sid, seeds, _variants())
+    try:
+        for vi, (name, ov) in enumerate(VARIANTS):
+            if not fast and name not in ("full", "static"):
+                continue
+            for si, seed in enumerate(seeds):
+                ref, _ = ref_run(path, seed, ov)
+                mine = res.run(vi * len(seeds) + si)
+                assert diff_results(ref, mine) == [], (name, seed)
+    finally:
+        res.close()
+
+
+def test_many_seeds_default(engine):
+    """32 seeds of default.yaml in one wave vs the reference (summaries + action logs)."""
+    path = GOLDEN_SCENARIOS[0]
+    sid = engine.load_scenario(path)
+    seeds = list(range(100, 132))
+    res = engine.run_batch(sid, seeds)
+    try:
+        for i in range(0, 32, 4):
+            ref, _ = ref_run(path, seeds[i])
+            assert diff_results(ref, res.run(i)) == []
+    finally:
+        res.close()
+
+
+@pytest.mark.parametrize("path", [GOLDEN_SCENARIOS[1], CONFIG_SCENARIOS[2], GOLDEN_SCENARIOS[0]])
+def test_per_completion_records(engine, path):
+    """keep_completions: every CompletionRecord (engine.hpp:47-57) bit-exact, plus the p999
+    extension against a nearest-rank restatement over the reference's window samples."""
+    sid = engine.load_scenario(path)
+    res = engine.run_batch(sid, [5], keep_completions=True)
+    try:
+        comps = res.completions(0)
+        run = res.run(0)
+        ref, rc = ref_run(path, 5, keep_completions=True)
+        ids = res.tenant_ids
+        for ti, tid in enumerate(ids):
+            mine = comps[comps[:, 0] == ti]
+            sel = rc["tenant"] == ti
+            assert len(mine) == sel.sum()
+            order = np.argsort(rc["seq"][sel], kind="stable")
+            for col, key in ((2, "done"), (3, "total"), (4, "compute"), (5, "transfer"), (6, "noise")):
+                a = rc[key][sel][order]
+                b = mine[:, col]
+                assert (a.view(np.uint64) == b.view(np.uint64)).all(), (tid, key)
+            ms = ref["summary"]["measure_start_s"]
+            win = rc["total"][sel][rc["done"][sel] >= ms]
+            if len(win):
+                assert run["tenants"][tid]["p999_ms"] == restate.nearest_rank(win.tolist(), 0.999)
+    finally:
+        res.close()
+
+
+def test_single_replica_api(engine):
+    """paper_2508_20274_b200.run_scenario mirrors engine::run_scenario (engine.hpp:117)."""
+    from paper_2508_20274_b200 import run_scenario
+
+    path = GOLDEN_SCENARIOS[1]
+    mine = run_scenario(path, seed=9)
+    ref, _ = ref_run(path, 9)
+    assert diff_results(ref, mine) == []
+
+
+def test_audit_invariants_hold_on_gpu_runs(engine):
+    """audit::audit_run (audit.cpp:52-122) over GPU logs == over the reference logs (both clean)."""
+    path = GOLDEN_SCENARIOS[0]
+    lib = oracle()
+    h = lib.ref_run(scenario_json(path), None, 3, 0)
+    issues = ctypes.c_void_p()
+    n = lib.ref_result_audit(h, scenario_json(path), None, ctypes.byref(issues))
+    lib.ref_result_free(h)
+    assert n == 0
+    sid = engine.load_scenario(path)
+    res = engine.run_batch(sid, [3])
+    acts = res.run(0)["actions"]
+    res.close()
+    last = {}
+    for a in acts:
+        if a["kind"] in ("guardrail_io_throttle", "guardrail_mps_quota", "move", "mig_up", "mig_down"):
+            if a["tenant"] in last:
+                assert a["obs_since_prev"] >= 256
+            last[a["tenant"]] = a["seq"]

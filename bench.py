@@ -212,10 +212,13 @@ def run_engine(args):
     barrier()
     wall_s = time.perf_counter() - t0
     clk = clocks.stop()
-    # per-seed focus rows + SLO-miss histogram (1e-3 bins) of the last step: the only cross-GPU data
+    # per-seed focus rows + SLO-miss histogram of the last step: the only cross-GPU data (8(e))
+    from paper_2508_20274_b200 import sharding
+
     focus = last.tenant_ids.index("ta")
-    rows = last.rows[:, focus]
-    hist = np.bincount(np.minimum((rows["miss_rate"] * 1000).astype(np.int64), 999), minlength=1000)
+    rows = np.stack([last.rows[:, focus]["p99_ms"], last.rows[:, focus]["miss_rate"],
+                     last.rows["throughput_hz"].sum(axis=1)], 1)
+    all_rows, hist, cis = sharding.reduce_rows(rows, dist, device="cuda")
     if dist:
         tt = torch.tensor([dev_ms, wall_s], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -223,12 +226,6 @@ def run_engine(args):
         cnt = torch.tensor([ticks, completions, arrivals, samples], dtype=torch.int64, device="cuda")
         dist.all_reduce(cnt)
         ticks, completions, arrivals, samples = [int(x) for x in cnt.tolist()]
-        h = torch.tensor(hist, dtype=torch.int64, device="cuda")
-        dist.all_reduce(h)
-        hist = h.cpu().numpy()
-        per_seed = torch.tensor(np.stack([rows["p99_ms"], rows["miss_rate"]], 1), device="cuda")
-        gathered = [torch.zeros_like(per_seed) for _ in range(world)]
-        dist.all_gather(gathered, per_seed)
     if rank != 0:
         last.close()
         if dist:
@@ -267,7 +264,8 @@ def run_engine(args):
                     "completions": completions, "arrivals": arrivals, "select_samples": samples},
         "clocks": clk,
         "cpu_baseline": cpu,
-        "miss_rate_histogram_nonzero_bins": int((hist > 0).sum()),
+        "outcome": {"focus_tenant": "ta", "seeds": int(len(all_rows)), "p99_ci_ms": cis[0], "miss_ci": cis[1],
+                    "miss_histogram_nonzero_bins": int((hist > 0).sum())},
     }
     print(json.dumps(line), flush=True)
     last.close()

@@ -230,7 +230,18 @@ struct TenantDyn {
     double pend_pause;
     uint64_t completed, n_window, misses;
     double sum_total;
+    int64_t base;   // offset of this tenant's records inside the replica's arrays
+    int32_t n_count, pad2;
+    double frac;    // sm_fraction of the current (gpu, profile) (engine.cpp:330-334)
 };
+
+MG_HD void prefetch_l1(const void* p) {
+#if defined(__CUDA_ARCH__)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+#else
+    (void)p;
+#endif
+}
 
 struct RootDyn {
     uint64_t active;  // tenant bitmask, iteration in id order == sorted root.active
@@ -305,6 +316,7 @@ struct Sim {
         s.t = t;
         s.key = (static_cast<uint64_t>(kind) << 48) | st.next_seq;
         st.next_seq += 1;
+        if (st.next_seq >= (1ull << 29)) st.error = kErrSeqOverflow;  // device event order uses 29 seq bits
     }
     MG_HD void cancel(int kind, int i) {
         Slot& s = slots[slot_index(kind, i)];
@@ -312,11 +324,12 @@ struct Sim {
         s.key = ~0ull;
     }
 
-    MG_HD double sm_fraction(int i) const {
+    MG_HD double calc_frac(int i) const {
         const PGpu& g = gpu_of(i);
         if (!g.mig_enabled) return 1.0;
         return fdiv_exact(static_cast<double>(profile_slices(st.td[i].profile)), static_cast<double>(g.total_slices));
     }
+    MG_HD double sm_fraction(int i) const { return st.td[i].frac; }
     MG_HD double eff_pcie_cap(int i) const {  // model.cpp:155-159
         const double base = spec(i).pcie_cap;
         if (!st.td[i].has_throttle) return base;
@@ -465,7 +478,7 @@ struct Sim {
         TenantDyn& d = st.td[i];
         const int cq_end = d.transferring ? d.tq_head - 1 : d.tq_head;
         if (d.computing || d.paused || d.cq_head >= cq_end) return;
-        const int64_t base = io.off[i];
+        const int64_t base = d.base;
         const int k = d.cq_head++;
         const double frac = sm_fraction(i);
         double service = fdiv_exact(fmul(spec(i).base_compute_ms, io.arr_mult[base + k]), frac);
@@ -510,7 +523,7 @@ struct Sim {
     MG_HD void start_transfer(int i) {
         TenantDyn& d = st.td[i];
         if (d.transferring || d.paused) return;
-        const int64_t base = io.off[i];
+        const int64_t base = d.base;
         while (d.tq_head < d.n_arrived) {
             const int k = d.tq_head++;
             const double bytes = io.arr_bytes[base + k];
@@ -534,9 +547,21 @@ struct Sim {
     // ---- event handlers (engine.cpp:422-782) ---------------------------------------------
     MG_HD void on_arrival(int i) {
         TenantDyn& d = st.td[i];
-        d.n_arrived += 1;
+        const int k = d.n_arrived;
+        if ((k & 15) == 0) {
+            // records are consumed in order; pull the next 128-B line of every per-request
+            // array into L1 a block ahead (arrays are 16-element aligned per tenant)
+            const int64_t o = d.base + k + 16;
+            prefetch_l1(io.arr_t + o);
+            prefetch_l1(io.arr_bytes + o);
+            prefetch_l1(io.arr_mult + o);
+            prefetch_l1(io.arr_noise + o);
+            prefetch_l1(io.irq_e + o);
+            prefetch_l1(io.req_transfer_ms + o);
+        }
+        d.n_arrived = k + 1;
         start_transfer(i);
-        if (d.n_arrived < io.count[i]) push(kEvArrival, i, io.arr_t[io.off[i] + d.n_arrived]);
+        if (d.n_arrived < d.n_count) push(kEvArrival, i, io.arr_t[d.base + d.n_arrived]);
     }
 
     MG_HD void on_transfer_complete(int i) {
@@ -553,7 +578,7 @@ struct Sim {
         d.remaining = 0.0;
         d.transferring = 0;
         const int k = d.tq_head - 1;
-        io.req_transfer_ms[io.off[i] + k] = fadd(d.transfer_ms, fmul(fsub(st.now, d.started_s), 1000.0));
+        io.req_transfer_ms[d.base + k] = fadd(d.transfer_ms, fmul(fsub(st.now, d.started_s), 1000.0));
         st.rd[r].active &= ~(1ull << i);
         d.grant = 0.0;
         reallocate_root(r);
@@ -564,7 +589,7 @@ struct Sim {
     MG_HD void on_compute_complete(int i) {
         TenantDyn& d = st.td[i];
         d.computing = 0;
-        const int64_t base = io.off[i];
+        const int64_t base = d.base;
         const int k = d.cur_compute;
         const double arrived = io.arr_t[base + k];
         double total = fmul(fsub(st.now, arrived), 1000.0);
@@ -608,7 +633,7 @@ struct Sim {
                     const TenantDyn& d = st.td[i];
                     if (d.host != S.roots[r].host || root_of(i) != r) continue;
                     if (d.transferring) backlog = fadd(backlog, d.remaining);
-                    const int64_t base = io.off[i];
+                    const int64_t base = d.base;
                     for (int k = d.tq_head; k < d.n_arrived; ++k) backlog = fadd(backlog, io.arr_bytes[base + k]);
                 }
                 if (in_first) io.backlog[2 * r] = fadd(io.backlog[2 * r], backlog);
@@ -758,6 +783,7 @@ struct Sim {
                 d.first = a.new_first;
                 d.count = a.new_count;
                 if (a.pin_cpu) d.cpu_pinned = 1;
+                d.frac = calc_frac(a.tenant);
                 break;
             }
             case kActMigUp:
@@ -770,6 +796,7 @@ struct Sim {
                 d.first = a.new_first;
                 d.count = a.new_count;
                 d.profile = a.new_profile;
+                d.frac = calc_frac(a.tenant);
                 break;
             }
             case kActRollback: {
@@ -795,6 +822,7 @@ struct Sim {
                 d.first = a.new_first;
                 d.count = a.new_count;
                 d.profile = a.new_profile;
+                d.frac = calc_frac(a.tenant);
                 break;
             }
             default:
@@ -1299,6 +1327,10 @@ struct Sim {
             d.first = p.first;
             d.count = p.count;
             d.profile = p.profile;
+            d.base = io.off[i];
+            d.n_count = io.count[i];
+            d.pad2 = 0;
+            d.frac = calc_frac(i);
             d.cpu_pinned = d.paused = d.transferring = d.computing = d.has_throttle = 0;
             d.n_arrived = d.tq_head = d.cq_head = d.cur_compute = d.irq_cursor = 0;
             d.pend_kind = d.has_pend = d.mt_p = d.mt_init = d.pad = 0;
@@ -1338,26 +1370,34 @@ struct Sim {
         push(kEvTick, 0, 1.0);
     }
 
+    // true if slot s holds the next event to run (engine.cpp:869-872)
+    MG_HD bool runnable(int s) const { return slots[s].key != ~0ull && !(slots[s].t > S.duration_s); }
+
+    // pop slot s and dispatch its event (engine.cpp:873-881)
+    MG_HD void dispatch(int s) {
+        const double t = slots[s].t;
+        const int kind = static_cast<int>(slots[s].key >> 48);
+        const int i = kind == kEvTick ? 0 : s - kind * T;
+        slots[s].t = k_inf();
+        slots[s].key = ~0ull;
+        st.now = t;
+        st.n_events += 1;
+        switch (kind) {
+            case kEvResume: on_resume(i); break;
+            case kEvExpire: on_guardrail_expire(i); break;
+            case kEvTransfer: on_transfer_complete(i); break;
+            case kEvCompute: on_compute_complete(i); break;
+            case kEvArrival: on_arrival(i); break;
+            default: on_tick(); break;
+        }
+    }
+
     MG_HD void run() {
         const int nslots = kEvKinds * T + 1;
         for (;;) {
             const int s = lanes.argmin_slot(slots, nslots);
-            const double t = slots[s].t;
-            if (slots[s].key == ~0ull || t > S.duration_s) break;
-            const int kind = s == kEvKinds * T ? kEvTick : s / T;
-            const int i = s == kEvKinds * T ? 0 : s % T;
-            slots[s].t = k_inf();
-            slots[s].key = ~0ull;
-            st.now = t;
-            st.n_events += 1;
-            switch (kind) {
-                case kEvResume: on_resume(i); break;
-                case kEvExpire: on_guardrail_expire(i); break;
-                case kEvTransfer: on_transfer_complete(i); break;
-                case kEvCompute: on_compute_complete(i); break;
-                case kEvArrival: on_arrival(i); break;
-                default: on_tick(); break;
-            }
+            if (!runnable(s)) break;
+            dispatch(s);
         }
         st.now = S.duration_s;
     }

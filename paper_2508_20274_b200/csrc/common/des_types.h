@@ -48,7 +48,13 @@ struct TenantOut {
 };
 
 // error codes (C-ABI return codes, include/migsim_b200.h)
-enum : int32_t { kErrNone = 0, kErrActionOverflow = 1, kErrPauseOverflow = 2, kErrArrivalOverflow = 3 };
+enum : int32_t {
+    kErrNone = 0,
+    kErrActionOverflow = 1,
+    kErrPauseOverflow = 2,
+    kErrArrivalOverflow = 3,
+    kErrSeqOverflow = 4,  // > 2^29 event pushes in one replica
+};
 
 struct ReplicaOut {
     int32_t n_actions, n_pauses, error, pad;

@@ -274,8 +274,8 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         CK(cudaMemsetAsync(A.gen_overflow.p, 0, sizeof(int32_t), s));
         CK(cudaEventRecord(g->ev[0], s));
         const int64_t nt = static_cast<int64_t>(w) * T;
-        mg::gen_times_kernel<<<static_cast<unsigned>((nt + 127) / 128), 128, 0, s>>>(A.scen.p, B, w);
-        mg::gen_marks_kernel<<<static_cast<unsigned>((4 * nt + 127) / 128), 128, 0, s>>>(A.scen.p, B, w);
+        mg::gen_times_kernel<<<static_cast<unsigned>((nt + 31) / 32), 32, 0, s>>>(A.scen.p, B, w);
+        mg::gen_marks_kernel<<<static_cast<unsigned>((4 * nt + 31) / 32), 32, 0, s>>>(A.scen.p, B, w);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[1], s));
         mg::des_kernel<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);

@@ -205,7 +205,8 @@ Packed pack(const ScenarioSpec& spec, const std::vector<Variant>& variants, doub
         // record capacity: mean count + cap_sigmas standard deviations of a renewal count
         const double mean = t.arrival_rate_hz * spec.duration_s;
         const double cvx = std::max(cv, 0.5);
-        P.cap[c] = static_cast<int64_t>(std::ceil(mean + cap_sigmas * cvx * std::sqrt(mean) + 64.0));
+        // (rounded to 16 records so every tenant's arrays start on a 128-byte line)
+        P.cap[c] = (static_cast<int64_t>(std::ceil(mean + cap_sigmas * cvx * std::sqrt(mean) + 64.0)) + 15) / 16 * 16;
     }
     for (size_t f = 0; f < spec.tenants.size(); ++f) P.file_order.push_back(canon_of_file[f]);
     int64_t s = 0;

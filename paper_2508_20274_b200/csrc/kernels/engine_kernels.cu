@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
                                                  WaveBuffers B, int n_rep, SimLayout L) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int r = blockIdx.x;
-    if (r >= n_rep || threadIdx.x != 0) return;
+    if (r >= n_rep) return;
     const int T = S->n_tenants;
     const PController& Cv = C[B.variant[r]];
     SimState& st = *reinterpret_cast<SimState*>(smem);
@@ -102,9 +102,46 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
         io.c_done = io.c_total = io.c_compute = io.c_transfer = io.c_noise = nullptr;
     }
     Sim<HostLanes> sim(*S, Cv, io, st, slots, HostLanes{});
-    sim.init(B.file_order, win, vwin);
-    sim.run();
-    sim.finish();
+    const int lane = threadIdx.x;
+    if (lane == 0) sim.init(B.file_order, win, vwin);
+    __syncwarp();
+    // Event loop: the warp finds the next event (argmin over the 5T+1 event slots, lane-parallel
+    // with a butterfly reduction), lane 0 runs the handler on the shared-memory state.
+    // Event times are >= 0, so the IEEE bit pattern orders them as unsigned integers; the total
+    // order (t, kind, seq) (engine.cpp:69-75) becomes (t_hi, t_lo, kind<<29 | seq) and the warp
+    // minimum is three redux.sync.min.u32 steps.  seq < 2^29 per replica is checked by the host.
+    const int nslots = kEvKinds * T + 1;
+    for (;;) {
+        uint32_t hi = 0xffffffffu, lo = 0xffffffffu, kq = 0xffffffffu;
+        int bi = -1;
+        for (int k = lane; k < nslots; k += 32) {
+            const uint64_t key = slots[k].key;
+            if (key == ~0ull) continue;
+            const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(slots[k].t));
+            const uint32_t h = static_cast<uint32_t>(tb >> 32), l = static_cast<uint32_t>(tb);
+            const uint32_t q = static_cast<uint32_t>((key >> 48) << 29) | static_cast<uint32_t>(key & 0x1fffffffu);
+            if (h < hi || (h == hi && (l < lo || (l == lo && q < kq)))) {
+                hi = h;
+                lo = l;
+                kq = q;
+                bi = k;
+            }
+        }
+        const uint32_t m1 = __reduce_min_sync(0xffffffffu, hi);
+        const uint32_t m2 = __reduce_min_sync(0xffffffffu, hi == m1 ? lo : 0xffffffffu);
+        const uint32_t m3 = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? kq : 0xffffffffu);
+        if (m1 == 0xffffffffu) break;  // no live event (every t >= 0 has a smaller high word)
+        const unsigned win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2 && kq == m3);
+        const int s = __shfl_sync(0xffffffffu, bi, __ffs(win) - 1);
+        const double t = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | m2));
+        if (t > S->duration_s) break;
+        if (lane == 0) sim.dispatch(s);
+        __syncwarp();
+    }
+    if (lane == 0) {
+        st.now = S->duration_s;
+        sim.finish();
+    }
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -1,0 +1,70 @@
+"""Seed sharding across GPUs and the end-of-run reduction.
+
+Replicas (variant x seed) share nothing (/root/reference/proj/src/harness.cpp:156-176), so ranks
+take contiguous seed blocks and run with no data-path communication.  At the end only two small
+collectives run (torch.distributed: NCCL over NVLink on the GPU box, gloo in the CPU tests):
+  * all-reduce (sum, int64) of the per-variant SLO-miss-rate histogram (1e-3 bins on [0, 1]);
+  * all-gather of the per-seed focus rows (p99, miss rate, summed throughput) so rank 0 can
+    build harness-identical confidence intervals by summing in seed order
+    (harness.cpp:32-43, 178-204).
+"""
+from __future__ import annotations
+
+import math
+from typing import List, Sequence, Tuple
+
+import numpy as np
+
+N_BINS = 1000
+
+
+def seed_block(rank: int, world: int, seeds_per_rank: int, seed_base: int = 1) -> List[int]:
+    """Contiguous block of seeds for `rank` (weak scaling: fixed seeds per rank)."""
+    start = seed_base + rank * seeds_per_rank
+    return list(range(start, start + seeds_per_rank))
+
+
+def split_seeds(seeds: Sequence[int], rank: int, world: int) -> List[int]:
+    """Contiguous block [r*N/P, (r+1)*N/P) of a fixed seed list (strong scaling)."""
+    n = len(seeds)
+    return list(seeds[rank * n // world:(rank + 1) * n // world])
+
+
+def miss_histogram(miss_rates: np.ndarray) -> np.ndarray:
+    """Exact integer histogram of per-seed miss rates, 1e-3 wide bins over [0, 1]."""
+    idx = np.minimum((np.asarray(miss_rates, np.float64) * N_BINS).astype(np.int64), N_BINS - 1)
+    return np.bincount(idx, minlength=N_BINS).astype(np.int64)
+
+
+def confidence_interval(values: Sequence[float]) -> Tuple[float, float]:
+    """harness::confidence_interval (harness.cpp:32-43): population sigma, summed in order."""
+    if len(values) == 0:
+        return 0.0, 0.0
+    n = float(len(values))
+    s = 0.0
+    for v in values:
+        s += float(v)
+    mean = s / n
+    ss = 0.0
+    for v in values:
+        ss += (float(v) - mean) * (float(v) - mean)
+    return mean, 1.96 * math.sqrt(ss / n) / math.sqrt(n)
+
+
+def reduce_rows(rows: np.ndarray, dist=None, device: str = "cpu"):
+    """rows: float64 [n_local_seeds, 3] = (p99_ms, miss_rate, throughput_hz) in seed order.
+
+    Returns (all_rows in global seed order, summed miss histogram, CIs) on every rank.
+    """
+    import torch
+
+    hist = torch.tensor(miss_histogram(rows[:, 1]), dtype=torch.int64, device=device)
+    local = torch.tensor(np.ascontiguousarray(rows, np.float64), device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(hist)
+        parts = [torch.zeros_like(local) for _ in range(dist.get_world_size())]
+        dist.all_gather(parts, local)
+        local = torch.cat(parts, 0)
+    all_rows = local.cpu().numpy()
+    cis = [confidence_interval(all_rows[:, k]) for k in range(3)]
+    return all_rows, hist.cpu().numpy(), cis

@@ -1,0 +1,61 @@
+"""Multi-rank (world_size 2, gloo on CPU) coverage of the seed sharding + end-of-run reduction
+used by bench.py for N>1 GPUs."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import restate
+from paper_2508_20274_b200 import sharding
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, rows_all, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seeds = sharding.seed_block(rank, world, len(rows_all) // world)
+    local = rows_all[np.array(seeds) - 1]
+    all_rows, hist, cis = sharding.reduce_rows(local, dist)
+    out[rank] = (all_rows, hist, cis)
+    dist.destroy_process_group()
+
+
+def test_seed_blocks_partition():
+    blocks = [sharding.seed_block(r, 4, 256) for r in range(4)]
+    assert sum(blocks, []) == list(range(1, 1025))
+    assert sum([sharding.split_seeds(list(range(10)), r, 3) for r in range(3)], []) == list(range(10))
+
+
+def test_two_rank_reduction_matches_single_process():
+    rng = np.random.default_rng(5)
+    rows = np.stack([rng.lognormal(2, 0.5, 64), rng.uniform(0, 0.2, 64), rng.uniform(100, 200, 64)], 1)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, rows, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    single_rows, single_hist, single_cis = sharding.reduce_rows(rows, None)
+    for r in range(2):
+        all_rows, hist, cis = out[r]
+        assert (all_rows == rows).all()
+        assert (hist == single_hist).all() and hist.sum() == 64
+        assert cis == single_cis
+        # CIs are harness-identical (population sigma, seed order)
+        assert cis[0] == restate.confidence_interval(rows[:, 0].tolist())

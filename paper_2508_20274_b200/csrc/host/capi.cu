@@ -21,6 +21,7 @@
 
 namespace mg {
 size_t select_smem_bytes();
+size_t gen_times_smem_bytes();
 }
 
 namespace {
@@ -274,8 +275,8 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         CK(cudaMemsetAsync(A.gen_overflow.p, 0, sizeof(int32_t), s));
         CK(cudaEventRecord(g->ev[0], s));
         const int64_t nt = static_cast<int64_t>(w) * T;
-        mg::gen_times_kernel<<<static_cast<unsigned>((nt + 31) / 32), 32, 0, s>>>(A.scen.p, B, w);
-        mg::gen_marks_kernel<<<static_cast<unsigned>((4 * nt + 31) / 32), 32, 0, s>>>(A.scen.p, B, w);
+        mg::gen_times_kernel<<<static_cast<unsigned>(nt), 32, mg::gen_times_smem_bytes(), s>>>(A.scen.p, B, w);
+        mg::gen_marks_kernel<<<static_cast<unsigned>(4 * nt), 32, 0, s>>>(A.scen.p, B, w);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[1], s));
         mg::des_kernel<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
@@ -857,8 +858,8 @@ int migsim_gpu_arrivals(migsim_gpu* g, int32_t scenario_id, uint64_t seed, int32
         B.gen_overflow = A.gen_overflow.p;
         B.cap_sum = P.cap_sum;
         B.any_irq_noise = P.any_irq_noise;
-        mg::gen_times_kernel<<<static_cast<unsigned>((T + 127) / 128), 128, 0, s>>>(A.scen.p, B, 1);
-        mg::gen_marks_kernel<<<static_cast<unsigned>((4 * T + 127) / 128), 128, 0, s>>>(A.scen.p, B, 1);
+        mg::gen_times_kernel<<<static_cast<unsigned>(T), 32, mg::gen_times_smem_bytes(), s>>>(A.scen.p, B, 1);
+        mg::gen_marks_kernel<<<static_cast<unsigned>(4 * T), 32, 0, s>>>(A.scen.p, B, 1);
         CK(cudaGetLastError());
         std::vector<int32_t> nk(T);
         CK(cudaMemcpyAsync(nk.data(), A.n_kept.p, 4 * T, cudaMemcpyDeviceToHost, s));

@@ -1,53 +1,58 @@
 // sm_100a kernels of the batched controller engine (see engine_kernels.cuh for the map to the
 // reference).  Build: nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false -lineinfo
 #include "engine_kernels.cuh"
+#include "gen_warp.cuh"
 
 namespace mg {
 
 // ---------------------------------------------------------------------------------------------
 // arrival-record generation
-__global__ void __launch_bounds__(128) gen_times_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep) {
+// one warp per (replica, tenant); blocks are tenant-major so neighbouring warps have equal rates
+__global__ void __launch_bounds__(32) gen_times_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    GammaSmem& g = *reinterpret_cast<GammaSmem*>(smem);
     const int T = S->n_tenants;
-    const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (g >= static_cast<int64_t>(n_rep) * T) return;
-    const int t = static_cast<int>(g / n_rep);  // tenant-major: a warp shares one tenant's rate
-    const int r = static_cast<int>(g % n_rep);
+    const int b = blockIdx.x;
+    if (b >= n_rep * T) return;
+    const int t = b / n_rep;
+    const int r = b % n_rep;
+    const int lane = threadIdx.x;
     const PTenant& p = S->tenants[t];
-    uint64_t mt[kMtN];
-    Mt64Ref rng{mt, 0};
-    rng.seed(substream_seed(B.seeds[r], p.name_hash, kArrivals));
     const int64_t base = static_cast<int64_t>(r) * B.cap_sum + B.off[t];
-    int32_t n_all = 0, n_kept = 0;
-    const bool ok = gen_times(rng, p, S->duration_s, B.t_all + base, B.arr_t + base, B.cap[t], &n_all, &n_kept);
-    B.n_all[r * T + t] = n_all;
-    B.n_kept[r * T + t] = n_kept;
-    if (!ok) atomicExch(B.gen_overflow, 1);
+    int32_t* n_all = B.n_all + r * T + t;
+    int32_t* n_kept = B.n_kept + r * T + t;
+    const bool ok = warp_gen_times(g, p, substream_seed(B.seeds[r], p.name_hash, kArrivals), S->duration_s,
+                                   B.t_all + base, B.arr_t + base, B.cap[t], n_all, n_kept, lane);
+    if (!ok && lane == 0) atomicExch(B.gen_overflow, 1);
 }
 
-__global__ void __launch_bounds__(128) gen_marks_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep) {
+// one warp per (replica, tenant, mark stream); purpose-major grid
+__global__ void __launch_bounds__(32) gen_marks_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep) {
+    __shared__ WarpMtSmem mt;
     const int T = S->n_tenants;
-    const int64_t per = static_cast<int64_t>(n_rep) * T;
-    const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (g >= 4 * per) return;
-    const int purpose = static_cast<int>(g / per);  // purpose-major: warps stay on one code path
-    const int64_t rest = g % per;
-    const int t = static_cast<int>(rest / n_rep);
-    const int r = static_cast<int>(rest % n_rep);
+    const int per = n_rep * T;
+    const int b = blockIdx.x;
+    if (b >= 4 * per) return;
+    const int purpose = b / per;
+    const int rest = b % per;
+    const int t = rest / n_rep;
+    const int r = rest % n_rep;
+    const int lane = threadIdx.x;
     const PTenant& p = S->tenants[t];
     const int64_t base = static_cast<int64_t>(r) * B.cap_sum + B.off[t];
-    uint64_t mt[kMtN];
-    Mt64Ref rng{mt, 0};
     if (purpose == kMarkIrq) {
         if (!B.any_irq_noise) return;
-        rng.seed(substream_seed(B.seeds[r], p.name_hash, kIrq));
-        gen_irq(rng, B.n_kept[r * T + t], B.irq_e + base);
+        warp_gen_marks(mt, kMarkIrq, p, substream_seed(B.seeds[r], p.name_hash, kIrq), nullptr,
+                       B.n_kept[r * T + t], false, B.irq_e + base, lane);
         return;
     }
     const uint64_t sp = purpose == kMarkSize ? kTransferSize : purpose == kMarkService ? kService : kNoise;
     double* out = purpose == kMarkSize ? B.arr_bytes : purpose == kMarkService ? B.arr_mult : B.arr_noise;
-    rng.seed(substream_seed(B.seeds[r], p.name_hash, sp));
-    gen_marks(rng, purpose, p, B.t_all + base, B.n_all[r * T + t], out + base);
+    warp_gen_marks(mt, purpose, p, substream_seed(B.seeds[r], p.name_hash, sp), B.t_all + base, B.n_all[r * T + t],
+                   p.sched.kind != kAlways, out + base, lane);
 }
+
+size_t gen_times_smem_bytes() { return sizeof(GammaSmem); }
 
 // ---------------------------------------------------------------------------------------------
 // replica DES: one warp per replica, working set in dynamic shared memory

@@ -1,0 +1,342 @@
+// Warp-cooperative arrival-record generation (device only).
+//
+// Same streams and the same arithmetic as the scalar restatement in common/arrivals.h and
+// common/rng.h (ArrivalGen::next, workload.cpp:129-157; libstdc++-13 <random>), reorganised so a
+// warp spends its time in parallel work:
+//  * mt19937_64 is advanced 312 outputs at a time by the whole warp: the twist of
+//    random.tcc:_M_gen_rand has two dependency-free phases (k < 156 reads only old words; k >= 156
+//    reads phase-1 words and old words), so each lane twists ~10 words per phase.
+//  * uniform-count streams (transfer size, noise, IRQ): one canonical per call, transformed
+//    lane-parallel and compacted through the schedule-thinning mask with ballots.
+//  * service (lognormal): each call starts with a fresh polar cache and consumes whole pairs, so
+//    pairs are aligned on even stream positions; accepted pairs are ranked with ballots.
+//  * arrival clock (gamma, Marsaglia-Tsang + pow boost): consumption is irregular, so the warp
+//    speculatively evaluates the polar transform for EVERY stream position (acc/ny/nx), lane 0
+//    walks the calls with cheap arithmetic only (the rare squeeze-rejection logs on demand), and
+//    the pow(u, 1/alpha) of every call is evaluated lane-parallel afterwards; lane 0 finally
+//    accumulates the clock in order (the FP sum order of workload.cpp:135).
+#pragma once
+
+#include "../common/arrivals.h"
+
+namespace mg {
+
+constexpr int kRing = 1024;       // canonical ring (positions)
+constexpr int kMaxCallsRound = 160;
+
+struct WarpMtSmem {
+    uint64_t x[kMtN];
+};
+
+__device__ __forceinline__ void warp_mt_seed(WarpMtSmem& m, uint64_t s, int lane) {
+    if (lane == 0) {
+        uint64_t prev = s;
+        m.x[0] = s;
+        for (int i = 1; i < kMtN; ++i) {
+            prev = 6364136223846793005ull * (prev ^ (prev >> 62)) + static_cast<uint64_t>(i);
+            m.x[i] = prev;
+        }
+    }
+    __syncwarp();
+}
+
+// Advance the state by one full twist (random.tcc _M_gen_rand), warp-parallel.
+__device__ __forceinline__ void warp_mt_twist(WarpMtSmem& m, int lane) {
+    uint64_t v[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int k = lane + 32 * j;
+        if (k < kMtN - kMtM) v[j] = mt_twist_one(m.x[k], m.x[k + 1], m.x[k + kMtM]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int k = lane + 32 * j;
+        if (k < kMtN - kMtM) m.x[k] = v[j];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int k = kMtN - kMtM + lane + 32 * j;
+        if (k < kMtN) v[j] = mt_twist_one(m.x[k], k == kMtN - 1 ? m.x[0] : m.x[k + 1], m.x[k - (kMtN - kMtM)]);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int k = kMtN - kMtM + lane + 32 * j;
+        if (k < kMtN) m.x[k] = v[j];
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ unsigned lanemask_lt(int lane) { return (1u << lane) - 1u; }
+
+// ---------------------------------------------------------------------------------------------
+// Uniform-count mark streams: purpose in {kMarkSize, kMarkService, kMarkNoise, kMarkIrq}.
+// n_calls: next() calls (or IRQ draws); t_all/thinned: schedule thinning of the calls.
+__device__ void warp_gen_marks(WarpMtSmem& m, int purpose, const PTenant& p, uint64_t seed_word, const double* t_all,
+                               int32_t n_calls, bool thinned, double* out, int lane) {
+    const bool draws = purpose == kMarkIrq || (purpose == kMarkSize && p.n_mix > 0) ||
+                       (purpose == kMarkService && p.has_service) || (purpose == kMarkNoise && p.has_noise);
+    if (!draws) {
+        // no RNG consumption at all: constant marks (workload.cpp:138-156)
+        const double v = purpose == kMarkService ? 1.0 : 0.0;
+        int64_t kept = 0;
+        for (int32_t c0 = 0; c0 < n_calls; c0 += 32) {
+            const int32_t c = c0 + lane;
+            const bool keep = c < n_calls && (!thinned || sched_active(p.sched, t_all[c]));
+            const unsigned mk = __ballot_sync(0xffffffffu, keep);
+            if (keep) out[kept + __popc(mk & lanemask_lt(lane))] = v;
+            kept += __popc(mk);
+        }
+        return;
+    }
+    warp_mt_seed(m, seed_word, lane);
+    int64_t call_base = 0, kept = 0;
+    while (call_base < n_calls) {
+        warp_mt_twist(m, lane);
+        if (purpose == kMarkService) {
+            // 156 aligned pairs per block; accepted pairs are the calls, in order
+            for (int j0 = 0; j0 < kMtN / 2 && call_base < n_calls; j0 += 32) {
+                const int j = j0 + lane;
+                double x = 0.0, y = 0.0, r2 = 2.0;
+                if (j < kMtN / 2) {
+                    x = fsub(fmul(2.0, canonical_from(mt_temper(m.x[2 * j]))), 1.0);
+                    y = fsub(fmul(2.0, canonical_from(mt_temper(m.x[2 * j + 1]))), 1.0);
+                    r2 = fadd(fmul(x, x), fmul(y, y));
+                }
+                const bool acc = j < kMtN / 2 && !(r2 > 1.0 || r2 == 0.0);
+                const unsigned ma = __ballot_sync(0xffffffffu, acc);
+                const int64_t call = call_base + __popc(ma & lanemask_lt(lane));
+                const bool valid = acc && call < n_calls;
+                const bool keep = valid && (!thinned || sched_active(p.sched, t_all[call]));
+                const unsigned mk = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const double mult = fsqrt(fdiv_exact(fmul(-2.0, gl_log(r2)), r2));
+                    const double n = fadd(fmul(fmul(y, mult), 1.0), 0.0);
+                    out[kept + __popc(mk & lanemask_lt(lane))] = gl_exp(fadd(fmul(p.svc_sigma, n), p.svc_mu));
+                }
+                kept += __popc(mk);
+                call_base += __popc(ma);
+            }
+        } else {
+            for (int j0 = 0; j0 < kMtN && call_base < n_calls; j0 += 32) {
+                const int j = j0 + lane;
+                const int64_t call = call_base + lane;
+                const bool valid = j < kMtN && call < n_calls;
+                const bool keep = valid && (!thinned || sched_active(p.sched, t_all[call]));
+                const unsigned mk = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const double c = canonical_from(mt_temper(m.x[j]));
+                    double v;
+                    if (purpose == kMarkSize) {
+                        const double pick = fadd(fmul(c, fsub(p.mix_cdf[p.n_mix - 1], 0.0)), 0.0);
+                        int idx = 0;
+                        while (idx + 1 < p.n_mix && pick >= p.mix_cdf[idx]) ++idx;
+                        v = p.mix_bytes[idx];
+                    } else if (purpose == kMarkNoise) {
+                        v = fdiv_exact(-gl_log(fsub(1.0, c)), p.noise_lambda);
+                    } else {
+                        v = -gl_log(fsub(1.0, c));
+                    }
+                    out[kept + __popc(mk & lanemask_lt(lane))] = v;
+                }
+                kept += __popc(mk);
+                const int take = kMtN - j0 < 32 ? kMtN - j0 : 32;
+                call_base += take;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Arrival clock stream (gamma renewal).
+struct GammaSmem {
+    WarpMtSmem mt;
+    double c[kRing];    // canonical at position p (ring)
+    double ny[kRing];   // y*mult if the pair starting at p is accepted
+    double nx[kRing];   // x*mult (the polar cache)
+    uint8_t acc[kRing];
+    double call_v[kMaxCallsRound];
+    int32_t call_q[kMaxCallsRound];
+    double call_g[kMaxCallsRound];
+    int32_t n_calls;
+};
+
+// Generate the next 312 canonicals at positions [gen_end, gen_end+312) and the speculative pair
+// transform for positions [gen_end-1, gen_end+311).
+__device__ __forceinline__ void gamma_fill(GammaSmem& g, int64_t gen_end, int lane) {
+    warp_mt_twist(g.mt, lane);
+    for (int j = lane; j < kMtN; j += 32) g.c[(gen_end + j) % kRing] = canonical_from(mt_temper(g.mt.x[j]));
+    __syncwarp();
+    for (int j = lane; j < kMtN; j += 32) {
+        const int64_t pos = gen_end - 1 + j;
+        if (pos < 0) continue;
+        const double x = fsub(fmul(2.0, g.c[pos % kRing]), 1.0);
+        const double y = fsub(fmul(2.0, g.c[(pos + 1) % kRing]), 1.0);
+        const double r2 = fadd(fmul(x, x), fmul(y, y));
+        const bool a = !(r2 > 1.0 || r2 == 0.0);
+        g.acc[pos % kRing] = a;
+        if (a) {
+            const double mult = fsqrt(fdiv_exact(fmul(-2.0, gl_log(r2)), r2));
+            g.ny[pos % kRing] = fmul(y, mult);
+            g.nx[pos % kRing] = fmul(x, mult);
+        }
+    }
+    __syncwarp();
+}
+
+// One gamma call's rejection loop (random.tcc:2366-2380) from stream position pos; returns
+// false if it would read past `limit` (positions with a complete pair transform).
+__device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaParams& gp, int64_t& pos, int64_t limit,
+                                                double& v_out, int32_t& q_out) {
+    int64_t p = pos;
+    bool cached = false;
+    double cache = 0.0, n, v, u;
+    for (;;) {
+        do {
+            if (cached) {
+                n = cache;
+                cached = false;
+            } else {
+                for (;;) {
+                    if (p + 1 >= limit) return false;
+                    if (g.acc[p % kRing]) break;
+                    p += 2;
+                }
+                n = g.ny[p % kRing];
+                cache = g.nx[p % kRing];
+                cached = true;
+                p += 2;
+            }
+            n = fadd(fmul(n, 1.0), 0.0);
+            v = fadd(1.0, fmul(gp.a2, n));
+        } while (v <= 0.0);
+        v = fmul(fmul(v, v), v);
+        if (p >= limit) return false;
+        u = g.c[p % kRing];
+        p += 1;
+        const double sq = fsub(1.0, fmul(fmul(fmul(fmul(0.0331, n), n), n), n));
+        if (!(u > sq)) break;
+        const double rhs = fadd(fmul(fmul(0.5, n), n), fmul(gp.a1, fadd(fsub(1.0, v), gl_log(v))));
+        if (!(gl_log(u) > rhs)) break;
+    }
+    int32_t q = -1;
+    if (!(gp.alpha == gp.malpha)) {
+        for (;;) {
+            if (p >= limit) return false;
+            const double u2 = g.c[p % kRing];
+            p += 1;
+            if (u2 != 0.0) break;
+        }
+        q = static_cast<int32_t>((p - 1) % kRing);
+    }
+    v_out = v;
+    q_out = q;
+    pos = p;
+    return true;
+}
+
+// Whole arrival-time stream of one (replica, tenant): t_all / t_kept and counts.
+__device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_word, double duration, double* t_all,
+                               double* t_kept, int64_t cap, int32_t* n_all_out, int32_t* n_kept_out, int lane) {
+    int64_t na = 0, nk = 0;
+    bool ok = true;
+    double clock = 0.0;
+    const bool thinned = p.sched.kind != kAlways;
+    if (p.deterministic) {
+        // clock += 1/lambda (workload.cpp:131-132): no RNG on this stream
+        if (lane == 0) {
+            for (;;) {
+                clock = fadd(clock, p.det_step);
+                if (clock >= duration) break;
+                if (na >= cap) {
+                    ok = false;
+                    break;
+                }
+                t_all[na++] = clock;
+                if (!thinned || sched_active(p.sched, clock)) t_kept[nk++] = clock;
+            }
+            *n_all_out = static_cast<int32_t>(na);
+            *n_kept_out = static_cast<int32_t>(nk);
+        }
+        return __shfl_sync(0xffffffffu, ok, 0);
+    }
+    const GammaParams gp = gamma_params(p);
+    warp_mt_seed(g.mt, seed_word, lane);
+    int64_t gen_end = 0;  // canonicals known for positions < gen_end
+    int64_t pos = 0;      // stream position of the next call
+    gamma_fill(g, gen_end, lane);
+    gen_end += kMtN;
+    bool done = false;
+    while (!done) {
+        // keep at least one full block of lookahead past the scan position
+        while (gen_end - pos < 2 * kMtN) {
+            gamma_fill(g, gen_end, lane);
+            gen_end += kMtN;
+        }
+        // lane 0: scan calls (cheap arithmetic) while the ring holds their positions
+        if (lane == 0) {
+            int32_t nc = 0;
+            const int64_t limit = gen_end - 1;  // pair transforms exist below gen_end-1
+            while (nc < kMaxCallsRound && pos + 1 < limit && limit - pos > 64) {
+                int64_t pp = pos;
+                double v;
+                int32_t q;
+                if (!gamma_scan_call(g, gp, pp, limit, v, q)) break;
+                g.call_v[nc] = v;
+                g.call_q[nc] = q;
+                ++nc;
+                pos = pp;
+            }
+            g.n_calls = nc;
+        }
+        __syncwarp();
+        pos = __shfl_sync(0xffffffffu, pos, 0);
+        const int32_t nc = g.n_calls;
+        // lane-parallel gap values: pow(u, 1/alpha) * a1 * v * beta (random.tcc:2382-2392)
+        for (int k = lane; k < nc; k += 32) {
+            const double v = g.call_v[k];
+            if (g.call_q[k] < 0) g.call_g[k] = fmul(fmul(gp.a1, v), gp.beta);
+            else g.call_g[k] = fmul(fmul(fmul(gl_pow(g.c[g.call_q[k]], gp.inv_alpha), gp.a1), v), gp.beta);
+        }
+        __syncwarp();
+        // lane 0: the clock is an ordered FP sum (workload.cpp:135)
+        if (lane == 0) {
+            for (int32_t k = 0; k < nc; ++k) {
+                clock = fadd(clock, g.call_g[k]);
+                if (clock >= duration) {
+                    done = true;
+                    break;
+                }
+                if (na >= cap) {
+                    ok = false;
+                    done = true;
+                    break;
+                }
+                t_all[na++] = clock;
+                if (!thinned || sched_active(p.sched, clock)) t_kept[nk++] = clock;
+            }
+        }
+        done = __shfl_sync(0xffffffffu, done, 0);
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!done && nc == 0) {
+            // one call needs more than the lookahead (~10^-200 probability): widen the window
+            // while the ring can hold it, otherwise report instead of reading stale positions
+            if (gen_end + kMtN - pos > kRing) {
+                ok = false;
+                done = true;
+            } else {
+                gamma_fill(g, gen_end, lane);
+                gen_end += kMtN;
+            }
+        }
+    }
+    if (lane == 0) {
+        *n_all_out = static_cast<int32_t>(na);
+        *n_kept_out = static_cast<int32_t>(nk);
+    }
+    return __shfl_sync(0xffffffffu, ok, 0);
+}
+
+}  // namespace mg

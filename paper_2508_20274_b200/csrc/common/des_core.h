@@ -268,11 +268,28 @@ struct SimState {
 // [Slot*(5T+1)] then, when `rings` is set, the controller windows [T*W] and validation windows [T*V].
 struct SimLayout {
     int64_t td, ctl, rd, slots, win, vwin, total;
+    // read-only scenario tables copied to shared memory (device only)
+    int64_t sc_tn, sc_gp, sc_rt, sc_iq, sc_hio, sc_ctrl, st;
 };
 MG_HD int64_t align16(int64_t x) { return (x + 15) & ~static_cast<int64_t>(15); }
-MG_HD SimLayout sim_layout(int T, int R, int W, int V, bool rings) {
+MG_HD SimLayout sim_layout(int T, int R, int W, int V, bool rings, int G = 0, int I = 0, int H = 0) {
     SimLayout L;
-    int64_t o = align16(sizeof(SimState));
+    int64_t o = 0;
+    L.sc_tn = o;
+    o = align16(o + static_cast<int64_t>(sizeof(PTenant)) * T);
+    L.sc_gp = o;
+    o = align16(o + static_cast<int64_t>(sizeof(PGpu)) * G);
+    L.sc_rt = o;
+    o = align16(o + static_cast<int64_t>(sizeof(PRoot)) * R);
+    L.sc_iq = o;
+    o = align16(o + static_cast<int64_t>(sizeof(PIrq)) * I);
+    L.sc_hio = o;
+    o = align16(o + 8ll * H);
+    L.sc_ctrl = o;
+    o = align16(o + static_cast<int64_t>(sizeof(PController)));
+    if (G == 0) o = 0;  // host harness: no copies
+    L.st = o;
+    o = align16(o + sizeof(SimState));
     L.td = o;
     o = align16(o + static_cast<int64_t>(sizeof(TenantDyn)) * T);
     L.ctl = o;
@@ -301,14 +318,27 @@ struct Sim {
     Slot* slots;  // 5*T + 1
     Lanes lanes;
     int T;
+    // Working-set arrays held as registers (not re-loaded from SimState) so that, after inlining
+    // into the kernel, the compiler sees shared-memory provenance and emits LDS/STS.
+    TenantDyn* td;
+    TenantCtl* ctl;
+    RootDyn* rd;
+    // Scenario tables; the kernel points these at shared-memory copies (see ScenCopy).
+    const PTenant* tn;
+    const PGpu* gp;
+    const PRoot* rt;
+    const PIrq* iq;
+    const double* hio;
 
-    MG_HD Sim(const PScenario& s, const PController& c, const ReplicaIO& i, SimState& state, Slot* sl, Lanes l)
-        : S(s), C(c), io(i), st(state), slots(sl), lanes(l), T(s.n_tenants) {}
+    MG_HD Sim(const PScenario& s, const PController& c, const ReplicaIO& i, SimState& state, Slot* sl, Lanes l,
+              TenantDyn* tdp, TenantCtl* ctlp, RootDyn* rdp)
+        : S(s), C(c), io(i), st(state), slots(sl), lanes(l), T(s.n_tenants), td(tdp), ctl(ctlp), rd(rdp),
+          tn(s.tenants), gp(s.gpus), rt(s.roots), iq(s.irq), hio(s.host_io_capacity) {}
 
     // ---- small helpers -------------------------------------------------------------------
-    MG_HD const PTenant& spec(int i) const { return S.tenants[i]; }
-    MG_HD const PGpu& gpu_of(int i) const { return S.gpus[st.td[i].gpu]; }
-    MG_HD int root_of(int i) const { return S.gpus[st.td[i].gpu].root; }
+    MG_HD const PTenant& spec(int i) const { return tn[i]; }
+    MG_HD const PGpu& gpu_of(int i) const { return gp[td[i].gpu]; }
+    MG_HD int root_of(int i) const { return gp[td[i].gpu].root; }
     MG_HD int slot_index(int kind, int i) const { return kind == kEvTick ? kEvKinds * T : kind * T + i; }
 
     MG_HD void push(int kind, int i, double t) {
@@ -327,55 +357,55 @@ struct Sim {
     MG_HD double calc_frac(int i) const {
         const PGpu& g = gpu_of(i);
         if (!g.mig_enabled) return 1.0;
-        return fdiv_exact(static_cast<double>(profile_slices(st.td[i].profile)), static_cast<double>(g.total_slices));
+        return fdiv_exact(static_cast<double>(profile_slices(td[i].profile)), static_cast<double>(g.total_slices));
     }
-    MG_HD double sm_fraction(int i) const { return st.td[i].frac; }
+    MG_HD double sm_fraction(int i) const { return td[i].frac; }
     MG_HD double eff_pcie_cap(int i) const {  // model.cpp:155-159
         const double base = spec(i).pcie_cap;
-        if (!st.td[i].has_throttle) return base;
-        const double thr = st.td[i].io_throttle;
+        if (!td[i].has_throttle) return base;
+        const double thr = td[i].io_throttle;
         return base > 0.0 ? (thr < base ? thr : base) : thr;
     }
     MG_HD uint64_t queue_len(int i) const {  // engine.cpp:245-247
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         const int cq_end = d.transferring ? d.tq_head - 1 : d.tq_head;
         return static_cast<uint64_t>(d.n_arrived - d.tq_head) + static_cast<uint64_t>(cq_end - d.cq_head) +
                static_cast<uint64_t>(d.transferring ? 1 : 0) + static_cast<uint64_t>(d.computing ? 1 : 0);
     }
     MG_HD double eff_host_io(int i) const {  // engine.cpp:336-344
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         if (d.paused) return 0.0;
         if (queue_len(i) == 0) return 0.0;
         double v = spec(i).host_io;
         if (d.has_throttle && d.io_throttle < v) v = d.io_throttle;
         return v;
     }
-    MG_HD double tenant_pcie(int i) const { return st.td[i].transferring ? st.td[i].grant : 0.0; }
+    MG_HD double tenant_pcie(int i) const { return td[i].transferring ? td[i].grant : 0.0; }
     MG_HD double tenant_sm_util(int i) const {  // engine.cpp:657-659
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         if (!(d.computing && !d.paused)) return 0.0;
         return fdiv_exact(fmul(fmul(spec(i).sm_demand, sm_fraction(i)), d.mps_quota), 100.0);
     }
     MG_HD double root_offered(int r) const {
         double s = 0.0;
-        for (uint64_t m = st.rd[r].active; m; m &= m - 1) s = fadd(s, st.td[ctz64(m)].grant);
+        for (uint64_t m = rd[r].active; m; m &= m - 1) s = fadd(s, td[ctz64(m)].grant);
         return s;
     }
     MG_HD double host_io(int h) const {
         double s = 0.0;
         for (int j = 0; j < T; ++j)
-            if (st.td[j].host == h) s = fadd(s, eff_host_io(j));
+            if (td[j].host == h) s = fadd(s, eff_host_io(j));
         return s;
     }
     MG_HD double gpu_sm_util(int h, int g) const {
         double s = 0.0;
         for (int j = 0; j < T; ++j)
-            if (st.td[j].host == h && st.td[j].gpu == g) s = fadd(s, tenant_sm_util(j));
+            if (td[j].host == h && td[j].gpu == g) s = fadd(s, tenant_sm_util(j));
         return s;
     }
     MG_HD bool irq_recent(int h, int core_group) const {  // engine.cpp:664-668
         for (int b = 0; b < S.n_irq; ++b) {
-            const PIrq& q = S.irq[b];
+            const PIrq& q = iq[b];
             if (q.host == h && q.core_group == core_group &&
                 sched_active_within(q.sched, fsub(st.now, C.irq_lookback_s), st.now))
                 return true;
@@ -392,8 +422,8 @@ struct Sim {
 
     // ---- fabric (fabric.cpp:31-87 via engine.cpp:312-347) ----------------------------------
     MG_HD void settle_root(int r) {
-        for (uint64_t m = st.rd[r].active; m; m &= m - 1) {
-            TenantDyn& d = st.td[ctz64(m)];
+        for (uint64_t m = rd[r].active; m; m &= m - 1) {
+            TenantDyn& d = td[ctz64(m)];
             const double dt = fsub(st.now, d.last_settle);
             if (dt > 0.0 && d.grant > 0.0) {
                 const double x = fsub(d.remaining, fmul(d.grant, dt));
@@ -405,8 +435,8 @@ struct Sim {
     }
 
     MG_HD void reallocate_root(int r) {
-        const uint64_t act = st.rd[r].active;
-        const double cap = S.roots[r].capacity;
+        const uint64_t act = rd[r].active;
+        const double cap = rt[r].capacity;
         if (act) {
             double wsum = 0.0;
             for (uint64_t m = act; m; m &= m - 1) wsum = fadd(wsum, spec(ctz64(m)).weight);
@@ -416,7 +446,7 @@ struct Sim {
                 const double share = fdiv_exact(fmul(cap, spec(i).weight), wsum);
                 const double c = eff_pcie_cap(i);
                 const double b = c > 0.0 ? (c < share ? c : share) : share;
-                st.td[i].grant = b;
+                td[i].grant = b;
                 granted = fadd(granted, b);
             }
             if (S.fabric_redistribute) {
@@ -426,14 +456,14 @@ struct Sim {
                     for (uint64_t m = act; m; m &= m - 1) {
                         const int i = ctz64(m);
                         const double c = eff_pcie_cap(i);
-                        if (!(c > 0.0) || st.td[i].grant < fsub(c, 1e-12)) open_w = fadd(open_w, spec(i).weight);
+                        if (!(c > 0.0) || td[i].grant < fsub(c, 1e-12)) open_w = fadd(open_w, spec(i).weight);
                     }
                     if (open_w <= 0.0) break;
                     double moved = 0.0;
                     for (uint64_t m = act; m; m &= m - 1) {
                         const int i = ctz64(m);
                         const double c = eff_pcie_cap(i);
-                        double& g = st.td[i].grant;
+                        double& g = td[i].grant;
                         if (c > 0.0 && g >= fsub(c, 1e-12)) continue;
                         double add = fdiv_exact(fmul(residual, spec(i).weight), open_w);
                         if (c > 0.0) {
@@ -450,7 +480,7 @@ struct Sim {
         }
         for (uint64_t m = act; m; m &= m - 1) {
             const int i = ctz64(m);
-            TenantDyn& d = st.td[i];
+            TenantDyn& d = td[i];
             d.last_settle = st.now;
             if (d.grant > 0.0 && d.remaining > kEpsBytes) {
                 push(kEvTransfer, i, fadd(st.now, fdiv_exact(d.remaining, d.grant)));
@@ -464,18 +494,18 @@ struct Sim {
 
     // ---- pipeline stages (engine.cpp:349-420) --------------------------------------------
     MG_HD bool irq_exposed(int i) const {
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         if (d.cpu_pinned) return false;
         const PGpu& g = gpu_of(i);
         for (int b = 0; b < S.n_irq; ++b) {
-            const PIrq& q = S.irq[b];
+            const PIrq& q = iq[b];
             if (q.host == d.host && q.core_group == g.core_group && sched_active(q.sched, st.now)) return true;
         }
         return false;
     }
 
     MG_HD void start_compute(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         const int cq_end = d.transferring ? d.tq_head - 1 : d.tq_head;
         if (d.computing || d.paused || d.cq_head >= cq_end) return;
         const int64_t base = d.base;
@@ -488,7 +518,7 @@ struct Sim {
             double pressure = 0.0;
             for (int j = 0; j < T; ++j) {
                 if (j == i) continue;
-                const TenantDyn& o = st.td[j];
+                const TenantDyn& o = td[j];
                 if (o.paused) continue;
                 if (o.host != d.host || o.gpu != d.gpu) continue;
                 if (!o.computing) continue;
@@ -499,7 +529,7 @@ struct Sim {
         double extra = io.arr_noise[base + k];
         if (irq_exposed(i)) {
             for (int b = 0; b < S.n_irq; ++b) {
-                const PIrq& q = S.irq[b];
+                const PIrq& q = iq[b];
                 if (q.host == d.host && q.core_group == g.core_group) {
                     if (q.extra_noise_ms > 0.0) {
                         const double e = io.irq_e[base + d.irq_cursor];
@@ -521,7 +551,7 @@ struct Sim {
     }
 
     MG_HD void start_transfer(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         if (d.transferring || d.paused) return;
         const int64_t base = d.base;
         while (d.tq_head < d.n_arrived) {
@@ -538,7 +568,7 @@ struct Sim {
             d.transferring = 1;
             const int r = root_of(i);
             settle_root(r);
-            st.rd[r].active |= 1ull << i;
+            rd[r].active |= 1ull << i;
             reallocate_root(r);
             return;
         }
@@ -546,7 +576,7 @@ struct Sim {
 
     // ---- event handlers (engine.cpp:422-782) ---------------------------------------------
     MG_HD void on_arrival(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         const int k = d.n_arrived;
         if ((k & 15) == 0) {
             // records are consumed in order; pull the next 128-B line of every per-request
@@ -565,7 +595,7 @@ struct Sim {
     }
 
     MG_HD void on_transfer_complete(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         const int r = root_of(i);
         settle_root(r);
         const double rem = d.remaining;
@@ -579,7 +609,7 @@ struct Sim {
         d.transferring = 0;
         const int k = d.tq_head - 1;
         io.req_transfer_ms[d.base + k] = fadd(d.transfer_ms, fmul(fsub(st.now, d.started_s), 1000.0));
-        st.rd[r].active &= ~(1ull << i);
+        rd[r].active &= ~(1ull << i);
         d.grant = 0.0;
         reallocate_root(r);
         start_compute(i);
@@ -587,7 +617,7 @@ struct Sim {
     }
 
     MG_HD void on_compute_complete(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         d.computing = 0;
         const int64_t base = d.base;
         const int k = d.cur_compute;
@@ -630,8 +660,8 @@ struct Sim {
                 if (!in_first && !in_last) continue;
                 double backlog = 0.0;
                 for (int i = 0; i < T; ++i) {
-                    const TenantDyn& d = st.td[i];
-                    if (d.host != S.roots[r].host || root_of(i) != r) continue;
+                    const TenantDyn& d = td[i];
+                    if (d.host != rt[r].host || root_of(i) != r) continue;
                     if (d.transferring) backlog = fadd(backlog, d.remaining);
                     const int64_t base = d.base;
                     for (int k = d.tq_head; k < d.n_arrived; ++k) backlog = fadd(backlog, io.arr_bytes[base + k]);
@@ -646,7 +676,7 @@ struct Sim {
 
     // ---- pause / actuation (engine.cpp:553-742) --------------------------------------------
     MG_HD double pause_draw(int i, double mean, double sd, double lo, double hi) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         Mt64Ref g{io.mt_pause + static_cast<int64_t>(i) * kMtN, d.mt_p};
         if (!d.mt_init) {
             g.seed(substream_seed(io.seed, spec(i).name_hash, kPause));
@@ -658,11 +688,11 @@ struct Sim {
     }
 
     MG_HD void pause_tenant(int i, double duration, int cause_kind) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         if (d.transferring) {
             const int r = root_of(i);
             settle_root(r);
-            st.rd[r].active &= ~(1ull << i);
+            rd[r].active &= ~(1ull << i);
             d.grant = 0.0;
             cancel(kEvTransfer, i);
             if (d.started_s >= 0.0) {
@@ -701,7 +731,7 @@ struct Sim {
     }
 
     MG_HD void on_resume(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         d.paused = 0;
         if (d.computing) {
             const double service = fdiv_exact(d.svc_ms, sm_fraction(i));
@@ -713,7 +743,7 @@ struct Sim {
             d.started_s = st.now;
             const int r = root_of(i);
             settle_root(r);
-            st.rd[r].active |= 1ull << i;
+            rd[r].active |= 1ull << i;
             reallocate_root(r);
         }
         start_transfer(i);
@@ -725,7 +755,7 @@ struct Sim {
     }
 
     MG_HD void on_guardrail_expire(int i) {
-        TenantDyn& d = st.td[i];
+        TenantDyn& d = td[i];
         int kind;
         if (d.has_throttle) {
             d.has_throttle = 0;
@@ -754,7 +784,7 @@ struct Sim {
     }
 
     MG_HD void apply_action(const Action& a) {
-        TenantDyn& tgt = st.td[a.target];
+        TenantDyn& tgt = td[a.target];
         switch (a.kind) {
             case kActIoThrottle: {
                 tgt.has_throttle = 1;
@@ -777,7 +807,7 @@ struct Sim {
             case kActMove: {
                 const double pause = pause_draw(a.tenant, 9.0, 3.0, 2.5, 15.0);
                 pause_tenant(a.tenant, pause, a.kind);
-                TenantDyn& d = st.td[a.tenant];
+                TenantDyn& d = td[a.tenant];
                 d.host = a.new_host;
                 d.gpu = a.new_gpu;
                 d.first = a.new_first;
@@ -790,7 +820,7 @@ struct Sim {
             case kActMigDown: {
                 const double pause = pause_draw(a.tenant, 18.0, 6.0, 5.0, 30.0);
                 pause_tenant(a.tenant, pause, a.kind);
-                TenantDyn& d = st.td[a.tenant];
+                TenantDyn& d = td[a.tenant];
                 d.host = a.new_host;
                 d.gpu = a.new_gpu;
                 d.first = a.new_first;
@@ -812,7 +842,7 @@ struct Sim {
                     on_action_applied(a.tenant, a.kind, st.now, 0.0);
                     break;
                 }
-                TenantDyn& d = st.td[a.tenant];
+                TenantDyn& d = td[a.tenant];
                 const bool profile_change = d.profile != a.new_profile;
                 const double pause = profile_change ? pause_draw(a.tenant, 18.0, 6.0, 5.0, 30.0)
                                                     : pause_draw(a.tenant, 9.0, 3.0, 2.5, 15.0);
@@ -873,7 +903,7 @@ struct Sim {
         if (a.kind == kActMove || a.kind == kActMigUp || a.kind == kActMigDown || a.kind == kActRollback) {
             if (!(a.kind == kActRollback && a.restore_throttle)) {
                 r->new_host = a.new_host;
-                r->new_gpu_id = a.new_gpu >= 0 ? S.gpus[a.new_gpu].id : -1;
+                r->new_gpu_id = a.new_gpu >= 0 ? gp[a.new_gpu].id : -1;
                 r->new_first = a.new_first;
                 r->new_end = a.new_first + a.new_count;
                 r->new_profile = a.new_profile;
@@ -905,12 +935,12 @@ struct Sim {
 
     // find_slice_run (controller.cpp:72-99); returns first or -1
     MG_HD int find_slice_run(int gidx, int host, int count, int prefer, int ignore) const {
-        const PGpu& g = S.gpus[gidx];
+        const PGpu& g = gp[gidx];
         if (count <= 0 || count > g.total_slices) return -1;
         uint64_t used = 0;
         for (int j = 0; j < T; ++j) {
             if (j == ignore) continue;
-            const TenantDyn& o = st.td[j];
+            const TenantDyn& o = td[j];
             if (o.host != host || o.gpu != gidx) continue;
             for (int s = o.first; s < o.first + o.count; ++s)
                 if (s >= 0 && s < g.total_slices) used |= 1ull << s;
@@ -929,15 +959,15 @@ struct Sim {
 
     // placement_score(...).total() (controller.cpp:101-123)
     MG_HD double placement_score(int i, int host, int gidx) const {
-        const PGpu& g = S.gpus[gidx];
-        const double root_cap = S.roots[g.root].capacity;
-        const double io_cap = S.host_io_capacity[host];
+        const PGpu& g = gp[gidx];
+        const double root_cap = rt[g.root].capacity;
+        const double io_cap = hio[host];
         double pcie = 0.0, numa = 0.0, irq = 0.0;
         for (int j = 0; j < T; ++j) {
             if (j == i) continue;
-            const TenantDyn& o = st.td[j];
+            const TenantDyn& o = td[j];
             if (o.host != host) continue;
-            const PGpu& og = S.gpus[o.gpu];
+            const PGpu& og = gp[o.gpu];
             if (spec(j).tclass == kBandwidthHeavy && og.root == g.root) pcie = fadd(pcie, fdiv_exact(tenant_pcie(j), root_cap));
             if (og.numa == g.numa) numa = fadd(numa, fdiv_exact(eff_host_io(j), io_cap));
         }
@@ -946,10 +976,10 @@ struct Sim {
     }
 
     MG_HD int diagnose(int i) const {  // controller.cpp:171-189
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         const int r = root_of(i);
-        const double root_util = fdiv_exact(root_offered(r), S.roots[r].capacity);
-        const double io_util = fdiv_exact(host_io(d.host), S.host_io_capacity[d.host]);
+        const double root_util = fdiv_exact(root_offered(r), rt[r].capacity);
+        const double io_util = fdiv_exact(host_io(d.host), hio[d.host]);
         if (root_util > C.diag_pcie_util_threshold || io_util > C.diag_host_io_threshold) return kDiagIo;
         const double gu = gpu_sm_util(d.host, d.gpu);
         const double own = tenant_sm_util(i);
@@ -972,18 +1002,18 @@ struct Sim {
     }
 
     MG_HD Action try_guardrail(int i, int diag) {  // controller.cpp:191-257
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         Action a = no_action();
         if (diag == kDiagIo) {
             const int myroot = root_of(i);
             const bool io_disjunct =
-                fdiv_exact(host_io(d.host), S.host_io_capacity[d.host]) > C.diag_host_io_threshold;
+                fdiv_exact(host_io(d.host), hio[d.host]) > C.diag_host_io_threshold;
             int off = -1;
             double best = 0.0;
             for (int j = 0; j < T; ++j) {
                 if (j == i) continue;
                 if (spec(j).tclass == kLatencySensitive) continue;
-                if (st.td[j].host != d.host) continue;
+                if (td[j].host != d.host) continue;
                 double load;
                 if (io_disjunct) {
                     load = eff_host_io(j);
@@ -997,7 +1027,7 @@ struct Sim {
                 }
             }
             if (off < 0 || best <= 0.0) return a;
-            if (st.td[off].has_throttle) return a;
+            if (td[off].has_throttle) return a;
             a.valid = 1;
             a.kind = kActIoThrottle;
             a.tenant = i;
@@ -1014,7 +1044,7 @@ struct Sim {
             for (int j = 0; j < T; ++j) {
                 if (j == i) continue;
                 if (spec(j).tclass == kLatencySensitive) continue;
-                if (st.td[j].host != d.host || st.td[j].gpu != d.gpu) continue;
+                if (td[j].host != d.host || td[j].gpu != d.gpu) continue;
                 const double u = tenant_sm_util(j);
                 if (u > best) {
                     best = u;
@@ -1022,7 +1052,7 @@ struct Sim {
                 }
             }
             if (off < 0) return a;
-            if (st.td[off].mps_quota < 100.0) return a;
+            if (td[off].mps_quota < 100.0) return a;
             a.valid = 1;
             a.kind = kActMpsQuota;
             a.tenant = i;
@@ -1036,31 +1066,31 @@ struct Sim {
     }
 
     MG_HD Action try_move(int i) {  // controller.cpp:259-303
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         Action a = no_action();
         const double current = placement_score(i, d.host, d.gpu);
         const double claim = spec(i).claim;
         int best_g = -1, best_first = -1;
         double best_score = 0.0;
         for (int g = 0; g < S.n_gpus; ++g) {
-            const PGpu& gp = S.gpus[g];
-            const int host = gp.host;
+            const PGpu& cg = gp[g];
+            const int host = cg.host;
             if (host == d.host && g == d.gpu) continue;
             const int run = find_slice_run(g, host, d.count, -1, i);
             if (run < 0) continue;
             double claims = claim;
             for (int j = 0; j < T; ++j) {
                 if (j == i) continue;
-                if (st.td[j].host != host) continue;
-                if (root_of(j) != gp.root) continue;
+                if (td[j].host != host) continue;
+                if (root_of(j) != cg.root) continue;
                 claims = fadd(claims, spec(j).claim);
             }
-            if (claims >= S.roots[gp.root].capacity) continue;
+            if (claims >= rt[cg.root].capacity) continue;
             const double score = placement_score(i, host, g);
             bool take = best_g < 0 || score < best_score;
             if (!take && score == best_score) {
-                const PGpu& bg = S.gpus[best_g];
-                take = host < bg.host || (host == bg.host && (gp.id < bg.id || (gp.id == bg.id && run < best_first)));
+                const PGpu& bg = gp[best_g];
+                take = host < bg.host || (host == bg.host && (cg.id < bg.id || (cg.id == bg.id && run < best_first)));
             }
             if (take) {
                 best_g = g;
@@ -1074,7 +1104,7 @@ struct Sim {
         a.kind = kActMove;
         a.tenant = i;
         a.target = i;
-        a.new_host = S.gpus[best_g].host;
+        a.new_host = gp[best_g].host;
         a.new_gpu = best_g;
         a.new_first = best_first;
         a.new_count = d.count;
@@ -1084,7 +1114,7 @@ struct Sim {
     }
 
     MG_HD Action try_mig_up(int i) {  // controller.cpp:305-319
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         Action a = no_action();
         if (d.profile + 1 >= kNumProfiles) return a;
         const int np = d.profile + 1;
@@ -1103,7 +1133,7 @@ struct Sim {
     }
 
     MG_HD Action try_relax(int i, TenantCtl& c) {  // controller.cpp:321-345
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         Action a = no_action();
         if (d.profile == 0) return a;
         if (c.relax_blocked >= 0 && d.profile == c.relax_blocked) return a;
@@ -1200,7 +1230,7 @@ struct Sim {
     }
 
     MG_HD void adopt(int i, TenantCtl& c, const Action& act, double p99, double t) {
-        const TenantDyn& d = st.td[i];
+        const TenantDyn& d = td[i];
         c.pre_p99_ms = p99;
         c.prior_host = d.host;
         c.prior_gpu = d.gpu;
@@ -1214,7 +1244,7 @@ struct Sim {
     }
 
     MG_HD Action on_observation(int i, double lat, double t, double arrived) {  // controller.cpp:489-603
-        TenantCtl& c = st.ctl[i];
+        TenantCtl& c = ctl[i];
         c.obs_total += 1;
         if (c.acted_ever) c.obs_since_action += 1;
         if (c.validating) {
@@ -1287,7 +1317,7 @@ struct Sim {
 
     // Controller::on_action_applied (controller.cpp:605-623)
     MG_HD void on_action_applied(int i, int kind, double t, double pause) {
-        TenantCtl& c = st.ctl[i];
+        TenantCtl& c = ctl[i];
         if (c.action_seq >= 0 && c.action_seq < st.n_actions && c.action_seq < io.action_cap)
             io.actions[c.action_seq].pause_s = pause;
         if (kind == kActRollback) {
@@ -1311,7 +1341,7 @@ struct Sim {
         st.n_events = 0;
         st.tick_index = 0;
         for (int r = 0; r < S.n_roots; ++r) {
-            st.rd[r].active = 0;
+            rd[r].active = 0;
             io.backlog[2 * r] = 0.0;
             io.backlog[2 * r + 1] = 0.0;
         }
@@ -1321,7 +1351,7 @@ struct Sim {
         }
         for (int i = 0; i < T; ++i) {
             const PTenant& p = spec(i);
-            TenantDyn& d = st.td[i];
+            TenantDyn& d = td[i];
             d.host = p.host;
             d.gpu = p.gpu;
             d.first = p.first;
@@ -1343,7 +1373,7 @@ struct Sim {
             d.pend_pause = 0.0;
             d.completed = d.n_window = d.misses = 0;
             d.sum_total = 0.0;
-            TenantCtl& c = st.ctl[i];
+            TenantCtl& c = ctl[i];
             const double tau = p.slo_tail_ms > 0.0 ? p.slo_tail_ms : C.tail_threshold_ms;
             c.trigger = tau;
             c.clear = fmul(C.hysteresis_clear_ratio, tau);
@@ -1404,14 +1434,14 @@ struct Sim {
 
     MG_HD void finish() {
         for (int i = 0; i < T; ++i) {
-            const TenantDyn& d = st.td[i];
+            const TenantDyn& d = td[i];
             TenantOut& o = io.tout[i];
             o.completed_total = d.completed;
             o.completed_window = d.n_window;
             o.window_misses = d.misses;
             o.sum_total_ms = d.sum_total;
             o.host = d.host;
-            o.gpu_id = S.gpus[d.gpu].id;
+            o.gpu_id = gp[d.gpu].id;
             o.first = d.first;
             o.profile = d.profile;
             o.cpu_pinned = d.cpu_pinned;

@@ -145,9 +145,10 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.R = R;
     const bool keep = opts.keep_completions != 0;
     // working-set layout: controller rings in shared memory when a replica stays under 96 KB
-    mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true);
+    const int G = P.scen.n_gpus, I = P.scen.n_irq, H = P.scen.n_hosts;
+    mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true, G, I, H);
     const bool rings_in_smem = L.total <= 96 * 1024;
-    if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false);
+    if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false, G, I, H);
     // wave size from free memory
     const size_t per_rep = static_cast<size_t>(P.cap_sum) * 8 * (8 + (keep ? 5 : 0)) + static_cast<size_t>(T) * 8 +
                            static_cast<size_t>(T) * mg::kMtN * 8 + static_cast<size_t>(action_cap) * sizeof(mg::ActionRec) * 2 +

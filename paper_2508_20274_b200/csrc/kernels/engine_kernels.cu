@@ -62,11 +62,25 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     const int r = blockIdx.x;
     if (r >= n_rep) return;
     const int T = S->n_tenants;
-    const PController& Cv = C[B.variant[r]];
-    SimState& st = *reinterpret_cast<SimState*>(smem);
-    st.td = reinterpret_cast<TenantDyn*>(smem + L.td);
-    st.ctl = reinterpret_cast<TenantCtl*>(smem + L.ctl);
-    st.rd = reinterpret_cast<RootDyn*>(smem + L.rd);
+    const int lane = threadIdx.x;
+    // read-only scenario tables -> shared memory (cooperative 8-B copies; all PODs are 8-B multiples)
+    auto copy16 = [&](int64_t dst_off, const void* src, int64_t bytes) {
+        const uint64_t* s8 = reinterpret_cast<const uint64_t*>(src);
+        uint64_t* d8 = reinterpret_cast<uint64_t*>(smem + dst_off);
+        for (int64_t k = lane; k < bytes / 8; k += 32) d8[k] = s8[k];
+    };
+    copy16(L.sc_tn, S->tenants, static_cast<int64_t>(sizeof(PTenant)) * T);
+    copy16(L.sc_gp, S->gpus, static_cast<int64_t>(sizeof(PGpu)) * S->n_gpus);
+    copy16(L.sc_rt, S->roots, static_cast<int64_t>(sizeof(PRoot)) * S->n_roots);
+    copy16(L.sc_iq, S->irq, static_cast<int64_t>(sizeof(PIrq)) * S->n_irq);
+    copy16(L.sc_hio, S->host_io_capacity, align16(8ll * S->n_hosts));
+    copy16(L.sc_ctrl, C + B.variant[r], static_cast<int64_t>(sizeof(PController)));
+    __syncwarp();
+    const PController& Cv = *reinterpret_cast<const PController*>(smem + L.sc_ctrl);
+    SimState& st = *reinterpret_cast<SimState*>(smem + L.st);
+    TenantDyn* td = reinterpret_cast<TenantDyn*>(smem + L.td);
+    TenantCtl* ctl = reinterpret_cast<TenantCtl*>(smem + L.ctl);
+    RootDyn* rd = reinterpret_cast<RootDyn*>(smem + L.rd);
     Slot* slots = reinterpret_cast<Slot*>(smem + L.slots);
     double* win;
     double* vwin;
@@ -106,9 +120,16 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     } else {
         io.c_done = io.c_total = io.c_compute = io.c_transfer = io.c_noise = nullptr;
     }
-    Sim<HostLanes> sim(*S, Cv, io, st, slots, HostLanes{});
-    const int lane = threadIdx.x;
-    if (lane == 0) sim.init(B.file_order, win, vwin);
+    Sim<HostLanes> sim(*S, Cv, io, st, slots, HostLanes{}, td, ctl, rd);
+    sim.tn = reinterpret_cast<const PTenant*>(smem + L.sc_tn);
+    sim.gp = reinterpret_cast<const PGpu*>(smem + L.sc_gp);
+    sim.rt = reinterpret_cast<const PRoot*>(smem + L.sc_rt);
+    sim.iq = reinterpret_cast<const PIrq*>(smem + L.sc_iq);
+    sim.hio = reinterpret_cast<const double*>(smem + L.sc_hio);
+    // The handlers run warp-uniformly: every lane executes the same instructions on the same
+    // shared-memory words (broadcast loads, same-value stores), so no lane-0 divergence region
+    // (BSSY/BSYNC) wraps the hot path.
+    sim.init(B.file_order, win, vwin);
     __syncwarp();
     // Event loop: the warp finds the next event (argmin over the 5T+1 event slots, lane-parallel
     // with a butterfly reduction), lane 0 runs the handler on the shared-memory state.
@@ -140,13 +161,11 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
         const int s = __shfl_sync(0xffffffffu, bi, __ffs(win) - 1);
         const double t = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | m2));
         if (t > S->duration_s) break;
-        if (lane == 0) sim.dispatch(s);
+        sim.dispatch(s);
         __syncwarp();
     }
-    if (lane == 0) {
-        st.now = S->duration_s;
-        sim.finish();
-    }
+    st.now = S->duration_s;
+    sim.finish();
 }
 
 // ---------------------------------------------------------------------------------------------

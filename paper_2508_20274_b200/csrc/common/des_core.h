@@ -230,6 +230,7 @@ struct TenantDyn {
     double pend_pause;
     uint64_t completed, n_window, misses;
     double sum_total;
+    double win_min, win_max;
     int64_t base;   // offset of this tenant's records inside the replica's arrays
     int32_t n_count, pad2;
     double frac;    // sm_fraction of the current (gpu, profile) (engine.cpp:330-334)
@@ -634,6 +635,8 @@ struct Sim {
             io.win_lat[base + static_cast<int64_t>(d.n_window)] = total;
             d.n_window += 1;
             d.sum_total = fadd(d.sum_total, total);
+            if (total < d.win_min) d.win_min = total;
+            if (total > d.win_max) d.win_max = total;
             if (total > spec(i).slo_tail_ms) d.misses += 1;
         }
         if (io.c_total) {
@@ -1373,6 +1376,8 @@ struct Sim {
             d.pend_pause = 0.0;
             d.completed = d.n_window = d.misses = 0;
             d.sum_total = 0.0;
+            d.win_min = k_inf();
+            d.win_max = -k_inf();
             TenantCtl& c = ctl[i];
             const double tau = p.slo_tail_ms > 0.0 ? p.slo_tail_ms : C.tail_threshold_ms;
             c.trigger = tau;
@@ -1445,6 +1450,8 @@ struct Sim {
             o.first = d.first;
             o.profile = d.profile;
             o.cpu_pinned = d.cpu_pinned;
+            o.win_min = d.win_min;
+            o.win_max = d.win_max;
             o.pad = 0;
         }
         io.rout->n_actions = st.n_actions;

@@ -45,6 +45,7 @@ struct TenantOut {
     double sum_total_ms;
     int32_t host, gpu_id, first, profile;
     int32_t cpu_pinned, pad;
+    double win_min, win_max;  // range of the measurement-window latencies (seeds the radix select)
 };
 
 // error codes (C-ABI return codes, include/migsim_b200.h)

@@ -168,199 +168,6 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     sim.finish();
 }
 
-// ---------------------------------------------------------------------------------------------
-// nearest-rank select (engine.cpp:800-816; rank = max(1, ceil(q n)), value at rank-1 of the sort)
-namespace {
-
-constexpr int kSelThreads = 256;
-constexpr int kDigitBits = 11;
-constexpr int kBins = 1 << kDigitBits;
-constexpr int kMaxQ = 4;
-constexpr int kGather = 1024;
-
-__device__ __forceinline__ uint64_t order_key(double x) {
-    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double key_value(uint64_t k) {
-    const uint64_t b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
-    return __longlong_as_double(static_cast<long long>(b));
-}
-
-struct SelectSmem {
-    uint32_t hist[kMaxQ][kBins];
-    uint64_t cand[kMaxQ][kGather];
-    uint32_t part[kSelThreads];
-    uint64_t prefix[kMaxQ];
-    int64_t kk[kMaxQ];
-    int64_t gsize[kMaxQ];
-    int32_t shift[kMaxQ];
-    int32_t owner[kMaxQ];  // quantile whose histogram this one shares (identical group)
-    uint32_t cnt[kMaxQ];
-    int32_t done[kMaxQ];
-    double result[kMaxQ];
-    int32_t gather;
-};
-
-__device__ __forceinline__ bool in_group(uint64_t key, uint64_t prefix, int shift) {
-    return shift >= 64 ? true : ((key ^ prefix) >> shift) == 0;
-}
-
-// One CTA selects ranks of nq quantiles over vals[0..n).
-__device__ void block_select(const double* __restrict__ vals, int64_t n, const double* qs, int nq, double* out,
-                             SelectSmem& sm) {
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    if (n <= 0) {
-        if (tid < nq) out[tid] = 0.0;
-        return;
-    }
-    if (tid < nq) {
-        int64_t rank = static_cast<int64_t>(ceil(__dmul_rn(qs[tid], static_cast<double>(n))));
-        if (rank < 1) rank = 1;
-        if (rank > n) rank = n;
-        sm.kk[tid] = rank - 1;
-        sm.prefix[tid] = 0;
-        sm.shift[tid] = 64;
-        sm.gsize[tid] = n;
-        sm.done[tid] = 0;
-    }
-    __syncthreads();
-    for (;;) {
-        // which quantiles still need a histogram pass; share identical groups
-        if (tid == 0) {
-            bool small = true;
-            for (int q = 0; q < nq; ++q) {
-                sm.owner[q] = q;
-                if (sm.done[q]) continue;
-                if (sm.shift[q] == 0 || sm.gsize[q] == 1) continue;
-                if (sm.gsize[q] > kGather) small = false;
-                for (int p = 0; p < q; ++p)
-                    if (!sm.done[p] && sm.prefix[p] == sm.prefix[q] && sm.shift[p] == sm.shift[q]) {
-                        sm.owner[q] = p;
-                        break;
-                    }
-            }
-            sm.gather = small;
-        }
-        __syncthreads();
-        if (sm.gather) break;
-        for (int q = 0; q < nq; ++q)
-            for (int b = tid; b < kBins; b += kSelThreads) sm.hist[q][b] = 0;
-        __syncthreads();
-        for (int64_t i = tid; i < n; i += kSelThreads) {
-            const uint64_t key = order_key(vals[i]);
-            for (int q = 0; q < nq; ++q) {
-                const int sh = sm.shift[q];
-                const bool active = !sm.done[q] && sm.owner[q] == q && sm.shift[q] > 0 && in_group(key, sm.prefix[q], sh);
-                const int d = sh < kDigitBits ? sh : kDigitBits;
-                const uint32_t digit = active ? static_cast<uint32_t>((key >> (sh - d)) & ((1u << d) - 1)) : 0xffffffffu;
-                // warp-aggregated histogram increments (skewed digits would serialize smem atomics)
-                const unsigned peers = __match_any_sync(__activemask(), digit);
-                if (active && lane == __ffs(peers) - 1) atomicAdd(&sm.hist[q][digit], __popc(peers));
-            }
-        }
-        __syncthreads();
-        // locate each quantile's digit: per-thread partial sums of 8 bins, block scan
-        for (int q = 0; q < nq; ++q) {
-            if (sm.done[q] || sm.shift[q] == 0 || sm.gsize[q] == 1) continue;
-            const int o = sm.owner[q];
-            constexpr int per = kBins / kSelThreads;
-            uint32_t s = 0;
-            for (int b = 0; b < per; ++b) s += sm.hist[o][tid * per + b];
-            sm.part[tid] = s;
-            __syncthreads();
-            if (tid == 0) {
-                int64_t acc = 0;
-                int th = 0;
-                while (th < kSelThreads - 1 && acc + sm.part[th] <= sm.kk[q]) acc += sm.part[th++];
-                int bin = th * per;
-                while (acc + sm.hist[o][bin] <= sm.kk[q]) acc += sm.hist[o][bin++];
-                const int sh = sm.shift[q];
-                const int d = sh < kDigitBits ? sh : kDigitBits;
-                sm.prefix[q] |= static_cast<uint64_t>(bin) << (sh - d);
-                sm.shift[q] = sh - d;
-                sm.kk[q] -= acc;
-                sm.gsize[q] = sm.hist[o][bin];
-            }
-            __syncthreads();
-        }
-    }
-    // resolve: fully determined groups directly, the rest by gathering the (small) group
-    if (tid < nq) sm.cnt[tid] = 0;
-    __syncthreads();
-    bool need_gather = false;
-    for (int q = 0; q < nq; ++q) need_gather |= !(sm.shift[q] == 0 || sm.gsize[q] == 1);
-    if (need_gather) {
-        for (int64_t i = tid; i < n; i += kSelThreads) {
-            const uint64_t key = order_key(vals[i]);
-            for (int q = 0; q < nq; ++q) {
-                if (sm.shift[q] == 0 || sm.gsize[q] == 1) continue;
-                if (in_group(key, sm.prefix[q], sm.shift[q])) {
-                    const uint32_t k = atomicAdd(&sm.cnt[q], 1u);
-                    if (k < kGather) sm.cand[q][k] = key;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    for (int q = 0; q < nq; ++q) {
-        if (sm.shift[q] == 0) {
-            if (tid == 0) sm.result[q] = key_value(sm.prefix[q]);
-        } else if (sm.gsize[q] == 1) {
-            // the single group member: find it
-            if (tid == 0) sm.result[q] = 0.0;
-            __syncthreads();
-            for (int64_t i = tid; i < n; i += kSelThreads) {
-                const uint64_t key = order_key(vals[i]);
-                if (in_group(key, sm.prefix[q], sm.shift[q])) sm.result[q] = key_value(key);
-            }
-        } else {
-            const int m = static_cast<int>(sm.gsize[q]);
-            for (int a = tid; a < m; a += kSelThreads) {
-                const uint64_t v = sm.cand[q][a];
-                int lt = 0, le = 0;
-                for (int b = 0; b < m; ++b) {
-                    lt += sm.cand[q][b] < v;
-                    le += sm.cand[q][b] <= v;
-                }
-                if (lt <= sm.kk[q] && sm.kk[q] < le) sm.result[q] = key_value(v);
-            }
-        }
-        __syncthreads();
-    }
-    if (tid < nq) out[tid] = sm.result[tid];
-}
-
-}  // namespace
-
-__global__ void __launch_bounds__(kSelThreads) select_kernel(WaveBuffers B, int T, int n_rep) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    SelectSmem& sm = *reinterpret_cast<SelectSmem*>(smem);
-    const int s = blockIdx.x;
-    if (s >= n_rep * T) return;
-    const int r = s / T, t = s % T;
-    const int64_t n = static_cast<int64_t>(B.tout[s].completed_window);
-    const double qs[kMaxQ] = {0.50, 0.95, 0.99, 0.999};
-    block_select(B.win_lat + static_cast<int64_t>(r) * B.cap_sum + B.off[t], n, qs, kMaxQ, B.quant + 4ll * s, sm);
-}
-
-__global__ void __launch_bounds__(kSelThreads) select_segments_kernel(const double* __restrict__ vals,
-                                                                      const int64_t* __restrict__ seg_off, int n_seg,
-                                                                      const double* __restrict__ qs, int nq,
-                                                                      double* __restrict__ out) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    SelectSmem& sm = *reinterpret_cast<SelectSmem*>(smem);
-    const int s = blockIdx.x;
-    if (s >= n_seg) return;
-    for (int q0 = 0; q0 < nq; q0 += kMaxQ) {
-        const int cnt = nq - q0 < kMaxQ ? nq - q0 : kMaxQ;
-        block_select(vals + seg_off[s], seg_off[s + 1] - seg_off[s], qs + q0, cnt, out + static_cast<int64_t>(s) * nq + q0, sm);
-        __syncthreads();
-    }
-}
-
-size_t select_smem_bytes() { return sizeof(SelectSmem); }
 
 // ---------------------------------------------------------------------------------------------
 __global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,

@@ -24,8 +24,12 @@
 
 #if defined(__CUDACC__)
 #define MG_HD __host__ __device__ __forceinline__
+// Rare paths.  Kept inline: out-of-line member calls force the simulator object (and every
+// member access on the hot path) into local memory, which measured 38% slower.
+#define MG_COLD __host__ __device__ __forceinline__
 #else
 #define MG_HD inline
+#define MG_COLD inline
 #endif
 
 namespace mg {

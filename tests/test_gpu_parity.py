@@ -6,12 +6,13 @@ rank -> indices bit-exact), SLO-miss and completion counts, end states, stabilit
 FP64 values are required bit-identical (stricter than the 1e-9 relative the spec allows).
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
 
 from oracle import restate
-from tests._libs import CONFIG_SCENARIOS, GOLDEN_SCENARIOS, diff_results, oracle, ref_run, scenario_json
+from tests._libs import CONFIG_DIR, CONFIG_SCENARIOS, GOLDEN_SCENARIOS, diff_results, oracle, ref_run, scenario_json
 
 pytestmark = pytest.mark.gpu
 
@@ -120,3 +121,48 @@ def test_audit_invariants_hold_on_gpu_runs(engine):
             if a["tenant"] in last:
                 assert a["obs_since_prev"] >= 256
             last[a["tenant"]] = a["seq"]
+
+
+def test_c5_64_tenants(engine):
+    """C5 shape: 64 tenants on 32 GPUs, exhaustive try_move scoring over all GPUs; controller rings
+    spill to global memory at this size."""
+    path = os.path.join(CONFIG_DIR, "c5_mc64.yaml")
+    sid = engine.load_scenario(path)
+    res = engine.run_batch(sid, [1])
+    try:
+        ref, _ = ref_run(path, 1)
+        assert len(ref["actions"]) > 100
+        assert diff_results(ref, res.run(0)) == []
+    finally:
+        res.close()
+
+
+@pytest.mark.parametrize("plan", ["e1", "e2"])
+def test_run_plan_matches_reference_harness(engine, plan):
+    """harness::run_plan (harness.cpp:114-216): per-seed focus p99/miss, summed throughput and the
+    population-sigma CIs summed in seed order, vs reference replicas aggregated by the restatement."""
+    path = GOLDEN_SCENARIOS[1]
+    exp = engine.run_plan(plan, path, seeds=3, seed_base=11)
+    from paper_2508_20274_b200 import ablation_variants, main_variants
+
+    variants = main_variants() if plan == "e1" else ablation_variants()
+    assert [v["name"] for v in exp["variants"]] == [v.name for v in variants]
+    assert exp["focus_tenant"] == "llm"
+    for v, ve in zip(variants, exp["variants"]):
+        ov = dict(enabled=v.enabled, enable_mig=v.enable_mig, enable_placement=v.enable_placement,
+                  enable_guardrails=v.enable_guardrails)
+        p99, miss, thr = [], [], []
+        for seed in (11, 12, 13):
+            ref, _ = ref_run(path, seed, ov)
+            t = ref["summary"]["tenants"]
+            p99.append(t["llm"]["p99_ms"])
+            miss.append(t["llm"]["miss_rate"])
+            s = 0.0
+            for tid in sorted(t):
+                s += t[tid]["throughput_hz"]
+            thr.append(s)
+        assert ve["seeds"] == [11, 12, 13]
+        assert ve["p99_ms"] == p99 and ve["miss_rate"] == miss and ve["throughput_hz"] == thr
+        for key, vals in (("p99_ci", p99), ("miss_ci", miss), ("throughput_ci", thr)):
+            m, h = restate.confidence_interval(vals)
+            assert ve[key] == {"mean": m, "half_width": h}

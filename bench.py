@@ -168,14 +168,18 @@ def run_engine(args):
     import torch
 
     dist = None
+    n_dev = torch.cuda.device_count()
+    device = local % max(n_dev, 1)
+    # NCCL over NVLink when every rank owns a GPU; gloo only when ranks share a device (test boxes)
+    coll_dev = "cuda" if n_dev >= world else "cpu"
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(device)
+        dist.init_process_group("nccl" if coll_dev == "cuda" else "gloo")
     from paper_2508_20274_b200 import Engine
 
-    eng = Engine(local)
+    eng = Engine(device)
     sid = eng.load_scenario(SCENARIO)
     T = len(eng.tenant_ids(sid))
     seeds = [1 + rank * SEEDS_PER_GPU + i for i in range(SEEDS_PER_GPU)]
@@ -187,7 +191,7 @@ def run_engine(args):
 
     for _ in range(args.warmup):
         eng.run_batch(sid, seeds).close()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(device)
     clocks.start()
     barrier()
     t0 = time.perf_counter()
@@ -216,14 +220,19 @@ def run_engine(args):
     from paper_2508_20274_b200 import sharding
 
     focus = last.tenant_ids.index("ta")
-    rows = np.stack([last.rows[:, focus]["p99_ms"], last.rows[:, focus]["miss_rate"],
-                     last.rows["throughput_hz"].sum(axis=1)], 1)
-    all_rows, hist, cis = sharding.reduce_rows(rows, dist, device="cuda")
+    thr = []
+    for run in last.rows:  # summed over tenants in id order, as harness.cpp:194-196
+        s = 0.0
+        for x in run["throughput_hz"]:
+            s += float(x)
+        thr.append(s)
+    rows = np.stack([last.rows[:, focus]["p99_ms"], last.rows[:, focus]["miss_rate"], np.array(thr)], 1)
+    all_rows, hist, cis = sharding.reduce_rows(rows, dist, device=coll_dev)
     if dist:
-        tt = torch.tensor([dev_ms, wall_s], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([dev_ms, wall_s], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dev_ms, wall_s = float(tt[0]), float(tt[1])
-        cnt = torch.tensor([ticks, completions, arrivals, samples], dtype=torch.int64, device="cuda")
+        cnt = torch.tensor([ticks, completions, arrivals, samples], dtype=torch.int64, device=coll_dev)
         dist.all_reduce(cnt)
         ticks, completions, arrivals, samples = [int(x) for x in cnt.tolist()]
     if rank != 0:

@@ -252,6 +252,22 @@ def run_engine(args):
         with open(tr_path) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     value = ticks / (dev_ms / 1000.0)
+    sat = None
+    if args.c4_seeds > 0:
+        # Secondary, outside the timed region: the saturated regime (BASELINE configs[3] shape,
+        # 4-variant ablation on default.yaml) where thousands of replicas fill every SM.
+        from paper_2508_20274_b200 import Variant
+
+        c4 = eng.load_scenario(os.path.join(ROOT, "tests", "golden", "scenarios", "default.yaml"))
+        vs = [Variant("static", False, False, False, False), Variant("mig-only", True, True, False, False),
+              Variant("placement-only", True, False, True, False), Variant("full", True, True, True, True)]
+        r4 = eng.run_batch(c4, list(range(1, args.c4_seeds + 1)), vs)
+        t4 = r4.timing
+        sat = {"workload": f"C4-shape ablation: default.yaml x 4 variants x {args.c4_seeds} seeds",
+               "replicas": int(t4["replicas"]), "tenant_ticks_per_s": t4["tenant_ticks"] / (t4["total_device_ms"] / 1e3),
+               "device_ms": t4["total_device_ms"], "des_ms": t4["des_ms"], "waves": int(t4["waves"]),
+               "completions_per_s": t4["completions"] / (t4["total_device_ms"] / 1e3)}
+        r4.close()
     h2d = 8 * SEEDS_PER_GPU + 4 * SEEDS_PER_GPU + 2 * (SEEDS_PER_GPU + 1) * 8
     d2h = int(last.timing["replicas"]) * (T * (48 + 32) + 24 + 16 * 2 * 8)
     cpu = None if args.no_cpu_baseline else cpu_baseline_sample()
@@ -275,6 +291,7 @@ def run_engine(args):
         "cpu_baseline": cpu,
         "outcome": {"focus_tenant": "ta", "seeds": int(len(all_rows)), "p99_ci_ms": cis[0], "miss_ci": cis[1],
                     "miss_histogram_nonzero_bins": int((hist > 0).sum())},
+        "saturated_regime": sat,
     }
     print(json.dumps(line), flush=True)
     last.close()
@@ -289,6 +306,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c4-seeds", type=int, default=1024, help="seeds of the secondary saturated-regime run (0: off)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -232,8 +232,9 @@ struct TenantDyn {
     double sum_total;
     double win_min, win_max;
     int64_t base;   // offset of this tenant's records inside the replica's arrays
-    int32_t n_count, pad2;
+    int32_t n_count, root;  // root: canonical PCIe root of the current placement
     double frac;    // sm_fraction of the current (gpu, profile) (engine.cpp:330-334)
+    double cap_eff; // effective_pcie_cap_Bps of the current throttle state (model.cpp:155-159)
 };
 
 MG_HD void prefetch_l1(const void* p) {
@@ -259,7 +260,7 @@ struct SimState {
     uint64_t next_seq;
     int32_t n_actions, n_pauses, error, next_action_seq;
     uint64_t n_events;
-    int32_t tick_index, pad;
+    int32_t tick_index, n_rare;  // n_rare: live resume/expire slots
     TenantDyn* td;   // n_tenants
     TenantCtl* ctl;  // n_tenants
     RootDyn* rd;     // n_roots
@@ -339,18 +340,34 @@ struct Sim {
     // ---- small helpers -------------------------------------------------------------------
     MG_HD const PTenant& spec(int i) const { return tn[i]; }
     MG_HD const PGpu& gpu_of(int i) const { return gp[td[i].gpu]; }
-    MG_HD int root_of(int i) const { return gp[td[i].gpu].root; }
-    MG_HD int slot_index(int kind, int i) const { return kind == kEvTick ? kEvKinds * T : kind * T + i; }
+    MG_HD int root_of(int i) const { return td[i].root; }
+    // placement or throttle changed: refresh the cached derived values
+    MG_HD void refresh(int i) {
+        TenantDyn& d = td[i];
+        d.root = gp[d.gpu].root;
+        d.frac = calc_frac(i);
+        const double base = spec(i).pcie_cap;
+        d.cap_eff = !d.has_throttle ? base : base > 0.0 ? (d.io_throttle < base ? d.io_throttle : base) : d.io_throttle;
+    }
+    // Slot layout: the three per-request kinds first, then the tick, then the rare kinds, so the
+    // device argmin scans only 3T+1 slots while no resume/expire event is live (st.n_rare == 0).
+    MG_HD int slot_base(int kind) const {
+        return kind == kEvCompute ? 0 : kind == kEvTransfer ? T : kind == kEvArrival ? 2 * T
+               : kind == kEvTick ? 3 * T : kind == kEvResume ? 3 * T + 1 : 4 * T + 1;
+    }
+    MG_HD int slot_index(int kind, int i) const { return slot_base(kind) + (kind == kEvTick ? 0 : i); }
+    MG_HD static bool rare_kind(int kind) { return kind == kEvResume || kind == kEvExpire; }
 
     MG_HD void push(int kind, int i, double t) {
         Slot& s = slots[slot_index(kind, i)];
+        if (rare_kind(kind) && s.key == ~0ull) st.n_rare += 1;
         s.t = t;
         s.key = (static_cast<uint64_t>(kind) << 48) | st.next_seq;
         st.next_seq += 1;
-        if (st.next_seq >= (1ull << 29)) st.error = kErrSeqOverflow;  // device event order uses 29 seq bits
     }
     MG_HD void cancel(int kind, int i) {
         Slot& s = slots[slot_index(kind, i)];
+        if (rare_kind(kind) && s.key != ~0ull) st.n_rare -= 1;
         s.t = k_inf();
         s.key = ~0ull;
     }
@@ -361,12 +378,7 @@ struct Sim {
         return fdiv_exact(static_cast<double>(profile_slices(td[i].profile)), static_cast<double>(g.total_slices));
     }
     MG_HD double sm_fraction(int i) const { return td[i].frac; }
-    MG_HD double eff_pcie_cap(int i) const {  // model.cpp:155-159
-        const double base = spec(i).pcie_cap;
-        if (!td[i].has_throttle) return base;
-        const double thr = td[i].io_throttle;
-        return base > 0.0 ? (thr < base ? thr : base) : thr;
-    }
+    MG_HD double eff_pcie_cap(int i) const { return td[i].cap_eff; }  // model.cpp:155-159, cached
     MG_HD uint64_t queue_len(int i) const {  // engine.cpp:245-247
         const TenantDyn& d = td[i];
         const int cq_end = d.transferring ? d.tq_head - 1 : d.tq_head;
@@ -762,6 +774,7 @@ struct Sim {
         int kind;
         if (d.has_throttle) {
             d.has_throttle = 0;
+            refresh(i);
             kind = kActIoThrottle;
         } else if (d.mps_quota < 100.0) {
             d.mps_quota = 100.0;
@@ -792,6 +805,7 @@ struct Sim {
             case kActIoThrottle: {
                 tgt.has_throttle = 1;
                 tgt.io_throttle = a.throttle_Bps;
+                refresh(a.target);
                 push(kEvExpire, a.target, a.expires_at_s);
                 if (tgt.transferring) {
                     const int r = root_of(a.target);
@@ -816,7 +830,7 @@ struct Sim {
                 d.first = a.new_first;
                 d.count = a.new_count;
                 if (a.pin_cpu) d.cpu_pinned = 1;
-                d.frac = calc_frac(a.tenant);
+                refresh(a.tenant);
                 break;
             }
             case kActMigUp:
@@ -829,12 +843,13 @@ struct Sim {
                 d.first = a.new_first;
                 d.count = a.new_count;
                 d.profile = a.new_profile;
-                d.frac = calc_frac(a.tenant);
+                refresh(a.tenant);
                 break;
             }
             case kActRollback: {
                 if (a.restore_throttle) {
                     tgt.has_throttle = 0;
+                    refresh(a.target);
                     tgt.mps_quota = 100.0;
                     cancel(kEvExpire, a.target);
                     if (tgt.transferring) {
@@ -855,7 +870,7 @@ struct Sim {
                 d.first = a.new_first;
                 d.count = a.new_count;
                 d.profile = a.new_profile;
-                d.frac = calc_frac(a.tenant);
+                refresh(a.tenant);
                 break;
             }
             default:
@@ -1342,6 +1357,7 @@ struct Sim {
         st.next_seq = 0;
         st.n_actions = st.n_pauses = st.error = st.next_action_seq = 0;
         st.n_events = 0;
+        st.n_rare = 0;
         st.tick_index = 0;
         for (int r = 0; r < S.n_roots; ++r) {
             rd[r].active = 0;
@@ -1362,13 +1378,12 @@ struct Sim {
             d.profile = p.profile;
             d.base = io.off[i];
             d.n_count = io.count[i];
-            d.pad2 = 0;
-            d.frac = calc_frac(i);
             d.cpu_pinned = d.paused = d.transferring = d.computing = d.has_throttle = 0;
             d.n_arrived = d.tq_head = d.cq_head = d.cur_compute = d.irq_cursor = 0;
             d.pend_kind = d.has_pend = d.mt_p = d.mt_init = d.pad = 0;
             d.mps_quota = 100.0;
             d.io_throttle = 0.0;
+            refresh(i);
             d.paused_until = 0.0;
             d.remaining = d.transfer_ms = d.last_settle = d.grant = 0.0;
             d.started_s = -1.0;
@@ -1412,7 +1427,8 @@ struct Sim {
     MG_HD void dispatch(int s) {
         const double t = slots[s].t;
         const int kind = static_cast<int>(slots[s].key >> 48);
-        const int i = kind == kEvTick ? 0 : s - kind * T;
+        const int i = kind == kEvTick ? 0 : s - slot_base(kind);
+        if (rare_kind(kind)) st.n_rare -= 1;
         slots[s].t = k_inf();
         slots[s].key = ~0ull;
         st.now = t;
@@ -1456,7 +1472,8 @@ struct Sim {
         }
         io.rout->n_actions = st.n_actions;
         io.rout->n_pauses = st.n_pauses;
-        io.rout->error = st.error;
+        // the device event order packs seq into 29 bits (engine_kernels.cu); never silently wrap
+        io.rout->error = st.next_seq >= (1ull << 29) ? kErrSeqOverflow : st.error;
         io.rout->pad = 0;
         io.rout->n_events = st.n_events;
     }

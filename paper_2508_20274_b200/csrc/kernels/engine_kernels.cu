@@ -136,10 +136,11 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     // Event times are >= 0, so the IEEE bit pattern orders them as unsigned integers; the total
     // order (t, kind, seq) (engine.cpp:69-75) becomes (t_hi, t_lo, kind<<29 | seq) and the warp
     // minimum is three redux.sync.min.u32 steps.  seq < 2^29 per replica is checked by the host.
-    const int nslots = kEvKinds * T + 1;
+    const int nslots_all = kEvKinds * T + 1, nslots_hot = 3 * T + 1;
     for (;;) {
         uint32_t hi = 0xffffffffu, lo = 0xffffffffu, kq = 0xffffffffu;
         int bi = -1;
+        const int nslots = st.n_rare ? nslots_all : nslots_hot;
         for (int k = lane; k < nslots; k += 32) {
             const uint64_t key = slots[k].key;
             if (key == ~0ull) continue;
@@ -154,10 +155,13 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
             }
         }
         const uint32_t m1 = __reduce_min_sync(0xffffffffu, hi);
-        const uint32_t m2 = __reduce_min_sync(0xffffffffu, hi == m1 ? lo : 0xffffffffu);
-        const uint32_t m3 = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? kq : 0xffffffffu);
         if (m1 == 0xffffffffu) break;  // no live event (every t >= 0 has a smaller high word)
-        const unsigned win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2 && kq == m3);
+        const uint32_t m2 = __reduce_min_sync(0xffffffffu, hi == m1 ? lo : 0xffffffffu);
+        unsigned win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2);
+        if (win & (win - 1)) {  // equal times: (kind, seq) decides
+            const uint32_t m3 = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? kq : 0xffffffffu);
+            win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2 && kq == m3);
+        }
         const int s = __shfl_sync(0xffffffffu, bi, __ffs(win) - 1);
         const double t = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | m2));
         if (t > S->duration_s) break;

@@ -245,6 +245,13 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     B.rings_in_smem = rings_in_smem;
     B.dwell = P.max_dwell;
     B.validation = P.max_validation;
+    DevBuf<unsigned long long> prof;
+    const bool want_prof = std::getenv("MIGSIM_PROFILE_EVENTS") != nullptr;
+    if (want_prof) {
+        prof.alloc(18);
+        CK(cudaMemsetAsync(prof.p, 0, 18 * 8, g->stream));
+        B.prof = prof.p;
+    }
 
     CK(cudaFuncSetAttribute(mg::des_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
     const size_t sel_smem = mg::select_smem_bytes();
@@ -292,6 +299,16 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         CK(cudaMemcpyAsync(nkept.data(), A.n_kept.p, sizeof(int32_t) * w * T, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         if (overflow) throw ParityGuard("arrival-record capacity exceeded");
+        if (want_prof) {
+            unsigned long long h[18];
+            CK(cudaMemcpy(h, prof.p, sizeof(h), cudaMemcpyDeviceToHost));
+            static const char* names[6] = {"resume", "expire", "transfer", "compute", "arrival", "tick"};
+            for (int k = 0; k < 6; ++k)
+                if (h[3 * k + 2])
+                    std::fprintf(stderr, "[event-profile] %-8s n=%llu pick=%.0f run=%.0f cycles/event\n", names[k],
+                                 h[3 * k + 2], static_cast<double>(h[3 * k]) / h[3 * k + 2],
+                                 static_cast<double>(h[3 * k + 1]) / h[3 * k + 2]);
+        }
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
         gen_ms += ms;

@@ -137,7 +137,14 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     // order (t, kind, seq) (engine.cpp:69-75) becomes (t_hi, t_lo, kind<<29 | seq) and the warp
     // minimum is three redux.sync.min.u32 steps.  seq < 2^29 per replica is checked by the host.
     const int nslots_all = kEvKinds * T + 1, nslots_hot = 3 * T + 1;
+#ifdef MG_PROFILE_EVENTS
+    // build-time instrumentation (make PROFILE=1): SM cycles spent choosing vs running events
+    unsigned long long c_pick[6] = {0, 0, 0, 0, 0, 0}, c_run[6] = {0, 0, 0, 0, 0, 0}, n_ev[6] = {0, 0, 0, 0, 0, 0};
+#endif
     for (;;) {
+#ifdef MG_PROFILE_EVENTS
+        const long long c0 = clock64();
+#endif
         uint32_t hi = 0xffffffffu, lo = 0xffffffffu, kq = 0xffffffffu;
         int bi = -1;
         const int nslots = st.n_rare ? nslots_all : nslots_hot;
@@ -165,11 +172,29 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
         const int s = __shfl_sync(0xffffffffu, bi, __ffs(win) - 1);
         const double t = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | m2));
         if (t > S->duration_s) break;
+#ifdef MG_PROFILE_EVENTS
+        const int kind = static_cast<int>(slots[s].key >> 48);
+        const long long c1 = clock64();
+#endif
         sim.dispatch(s);
         __syncwarp();
+#ifdef MG_PROFILE_EVENTS
+        const long long c2 = clock64();
+        c_pick[kind] += c1 - c0;
+        c_run[kind] += c2 - c1;
+        n_ev[kind] += 1;
+#endif
     }
     st.now = S->duration_s;
     sim.finish();
+#ifdef MG_PROFILE_EVENTS
+    if (lane == 0 && B.prof)
+        for (int k = 0; k < 6; ++k) {
+            atomicAdd(B.prof + 3 * k + 0, c_pick[k]);
+            atomicAdd(B.prof + 3 * k + 1, c_run[k]);
+            atomicAdd(B.prof + 3 * k + 2, n_ev[k]);
+        }
+#endif
 }
 
 

@@ -41,6 +41,7 @@ struct WaveBuffers {
     int32_t action_cap, pause_cap;
     int32_t any_irq_noise, rings_in_smem;
     int32_t dwell, validation;  // ring strides (max over variants)
+    unsigned long long* prof;   // [6][3] event-loop cycle counters (MG_PROFILE_EVENTS builds only)
 };
 
 __global__ void gen_times_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep);

@@ -230,9 +230,18 @@ __device__ void block_select(const double* __restrict__ vals, int64_t n, bool ha
         for (int b = 0; b < per; ++b) s += sm.hist[tid * per + b];
         const int64_t lo = block_excl_scan(s, sm.wsum);
         const int64_t hi = lo + s;
+        // snapshot the quantile states before any owner rewrites them: a thread must never pair
+        // another thread's fresh rank with the stale prefix/shift of the same quantile
+        bool member[kMaxQ];
+        int64_t rank_of[kMaxQ];
         for (int p = 0; p < nq; ++p) {
-            if (sm.qdone[p] || sm.qprefix[p] != prefix || sm.qshift[p] != sh) continue;
-            const int64_t rk = sm.qrank[p];
+            member[p] = !sm.qdone[p] && sm.qprefix[p] == prefix && sm.qshift[p] == sh;
+            rank_of[p] = sm.qrank[p];
+        }
+        __syncthreads();
+        for (int p = 0; p < nq; ++p) {
+            if (!member[p]) continue;
+            const int64_t rk = rank_of[p];
             if (rk >= lo && rk < hi) {
                 int64_t acc = lo;
                 int bin = tid * per;

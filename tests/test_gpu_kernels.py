@@ -80,3 +80,25 @@ def test_select_matches_nearest_rank(engine):
             expect = restate.nearest_rank(s.tolist(), q) if len(s) else 0.0
             assert v == expect, (len(s), q, v, expect)
     assert ms > 0
+
+
+def test_select_many_segments_shared_groups(engine):
+    """Many large segments where several quantiles land in the same digit group (bimodal data with
+    heavy ties, like a deterministic-service tenant's latencies): exercises concurrent refinement
+    of quantiles that share a group -- the pattern that once raced on the shared quantile state."""
+    rng = np.random.default_rng(558)
+    segs = []
+    for k in range(300):
+        n = int(rng.integers(4097, 30_000))
+        lo = np.round(2.45 + rng.exponential(0.01, n), 4)
+        hi = np.round(7.6 + rng.exponential(0.5, n), 3)
+        pick = rng.random(n) < rng.choice([0.005, 0.01, 0.012, 0.02])
+        segs.append(np.where(pick, hi, lo))
+    qs = [0.5, 0.95, 0.99, 0.999]
+    out, _ = engine.select(segs, qs)
+    for s, row in zip(segs, out):
+        srt = np.sort(s)
+        n = len(s)
+        for q, v in zip(qs, row):
+            r = min(max(int(np.ceil(q * n)), 1), n) - 1
+            assert v == srt[r], (n, q, v, srt[r])

@@ -255,12 +255,11 @@ struct Slot {
 };
 
 // Everything one replica mutates; lives in shared memory on the device.
+// (The clock, the push counter and the live-slot masks are Sim members instead: registers on
+// the device.)
 struct SimState {
-    double now;
-    uint64_t next_seq;
     int32_t n_actions, n_pauses, error, next_action_seq;
-    uint64_t n_events;
-    int32_t tick_index, n_rare;  // n_rare: live resume/expire slots
+    int32_t tick_index, pad;
     TenantDyn* td;   // n_tenants
     TenantCtl* ctl;  // n_tenants
     RootDyn* rd;     // n_roots
@@ -317,9 +316,12 @@ struct Sim {
     const PController& C;
     ReplicaIO io;
     SimState& st;
-    Slot* slots;  // 5*T + 1
-    Lanes lanes;
+    Lanes lanes;  // owns the 5T+1 event slots (host: an array; device: lane registers or smem)
     int T;
+    // per-event scalars kept out of shared memory (registers once inlined into the kernel)
+    double now;
+    uint64_t next_seq, n_events;
+    uint64_t live_resume, live_expire;  // tenants with a live resume / guardrail-expire event
     // Working-set arrays held as registers (not re-loaded from SimState) so that, after inlining
     // into the kernel, the compiler sees shared-memory provenance and emits LDS/STS.
     TenantDyn* td;
@@ -332,10 +334,11 @@ struct Sim {
     const PIrq* iq;
     const double* hio;
 
-    MG_HD Sim(const PScenario& s, const PController& c, const ReplicaIO& i, SimState& state, Slot* sl, Lanes l,
+    MG_HD Sim(const PScenario& s, const PController& c, const ReplicaIO& i, SimState& state, Lanes l,
               TenantDyn* tdp, TenantCtl* ctlp, RootDyn* rdp)
-        : S(s), C(c), io(i), st(state), slots(sl), lanes(l), T(s.n_tenants), td(tdp), ctl(ctlp), rd(rdp),
-          tn(s.tenants), gp(s.gpus), rt(s.roots), iq(s.irq), hio(s.host_io_capacity) {}
+        : S(s), C(c), io(i), st(state), lanes(l), T(s.n_tenants), now(0.0), next_seq(0), n_events(0),
+          live_resume(0), live_expire(0), td(tdp), ctl(ctlp), rd(rdp), tn(s.tenants), gp(s.gpus), rt(s.roots),
+          iq(s.irq), hio(s.host_io_capacity) {}
 
     // ---- small helpers -------------------------------------------------------------------
     MG_HD const PTenant& spec(int i) const { return tn[i]; }
@@ -350,26 +353,27 @@ struct Sim {
         d.cap_eff = !d.has_throttle ? base : base > 0.0 ? (d.io_throttle < base ? d.io_throttle : base) : d.io_throttle;
     }
     // Slot layout: the three per-request kinds first, then the tick, then the rare kinds, so the
-    // device argmin scans only 3T+1 slots while no resume/expire event is live (st.n_rare == 0).
+    // device argmin scans only 3T+1 slots while no resume/expire event is live (any_rare() false).
     MG_HD int slot_base(int kind) const {
         return kind == kEvCompute ? 0 : kind == kEvTransfer ? T : kind == kEvArrival ? 2 * T
                : kind == kEvTick ? 3 * T : kind == kEvResume ? 3 * T + 1 : 4 * T + 1;
     }
     MG_HD int slot_index(int kind, int i) const { return slot_base(kind) + (kind == kEvTick ? 0 : i); }
     MG_HD static bool rare_kind(int kind) { return kind == kEvResume || kind == kEvExpire; }
+    MG_HD bool any_rare() const { return (live_resume | live_expire) != 0; }
+    MG_HD void mark_rare(int kind, int i, bool live) {
+        uint64_t& m = kind == kEvResume ? live_resume : live_expire;
+        m = live ? (m | (1ull << i)) : (m & ~(1ull << i));
+    }
 
     MG_HD void push(int kind, int i, double t) {
-        Slot& s = slots[slot_index(kind, i)];
-        if (rare_kind(kind) && s.key == ~0ull) st.n_rare += 1;
-        s.t = t;
-        s.key = (static_cast<uint64_t>(kind) << 48) | st.next_seq;
-        st.next_seq += 1;
+        if (rare_kind(kind)) mark_rare(kind, i, true);
+        lanes.set(slot_index(kind, i), t, (static_cast<uint64_t>(kind) << 48) | next_seq);
+        next_seq += 1;
     }
     MG_HD void cancel(int kind, int i) {
-        Slot& s = slots[slot_index(kind, i)];
-        if (rare_kind(kind) && s.key != ~0ull) st.n_rare -= 1;
-        s.t = k_inf();
-        s.key = ~0ull;
+        if (rare_kind(kind)) mark_rare(kind, i, false);
+        lanes.clear(slot_index(kind, i));
     }
 
     MG_HD double calc_frac(int i) const {
@@ -420,7 +424,7 @@ struct Sim {
         for (int b = 0; b < S.n_irq; ++b) {
             const PIrq& q = iq[b];
             if (q.host == h && q.core_group == core_group &&
-                sched_active_within(q.sched, fsub(st.now, C.irq_lookback_s), st.now))
+                sched_active_within(q.sched, fsub(now, C.irq_lookback_s), now))
                 return true;
         }
         return false;
@@ -437,13 +441,13 @@ struct Sim {
     MG_HD void settle_root(int r) {
         for (uint64_t m = rd[r].active; m; m &= m - 1) {
             TenantDyn& d = td[ctz64(m)];
-            const double dt = fsub(st.now, d.last_settle);
+            const double dt = fsub(now, d.last_settle);
             if (dt > 0.0 && d.grant > 0.0) {
                 const double x = fsub(d.remaining, fmul(d.grant, dt));
                 d.remaining = 0.0 < x ? x : 0.0;
                 if (d.remaining < kEpsBytes) d.remaining = 0.0;
             }
-            d.last_settle = st.now;
+            d.last_settle = now;
         }
     }
 
@@ -494,11 +498,11 @@ struct Sim {
         for (uint64_t m = act; m; m &= m - 1) {
             const int i = ctz64(m);
             TenantDyn& d = td[i];
-            d.last_settle = st.now;
+            d.last_settle = now;
             if (d.grant > 0.0 && d.remaining > kEpsBytes) {
-                push(kEvTransfer, i, fadd(st.now, fdiv_exact(d.remaining, d.grant)));
+                push(kEvTransfer, i, fadd(now, fdiv_exact(d.remaining, d.grant)));
             } else if (d.remaining <= kEpsBytes) {
-                push(kEvTransfer, i, st.now);
+                push(kEvTransfer, i, now);
             } else {
                 cancel(kEvTransfer, i);  // starved: generation bumped, nothing scheduled
             }
@@ -512,7 +516,7 @@ struct Sim {
         const PGpu& g = gpu_of(i);
         for (int b = 0; b < S.n_irq; ++b) {
             const PIrq& q = iq[b];
-            if (q.host == d.host && q.core_group == g.core_group && sched_active(q.sched, st.now)) return true;
+            if (q.host == d.host && q.core_group == g.core_group && sched_active(q.sched, now)) return true;
         }
         return false;
     }
@@ -559,7 +563,7 @@ struct Sim {
         d.extra_ms = extra;
         d.compute_done_ms = 0.0;
         d.cur_transfer_ms = io.req_transfer_ms[base + k];
-        d.compute_end = fadd(st.now, fdiv_exact(fadd(service, extra), 1000.0));
+        d.compute_end = fadd(now, fdiv_exact(fadd(service, extra), 1000.0));
         push(kEvCompute, i, d.compute_end);
     }
 
@@ -575,7 +579,7 @@ struct Sim {
                 start_compute(i);
                 continue;
             }
-            d.started_s = st.now;
+            d.started_s = now;
             d.remaining = bytes;
             d.transfer_ms = 0.0;
             d.transferring = 1;
@@ -613,7 +617,7 @@ struct Sim {
         settle_root(r);
         const double rem = d.remaining;
         const bool done =
-            rem <= kEpsBytes || (d.grant > 0.0 && fadd(st.now, fdiv_exact(rem, d.grant)) <= st.now);
+            rem <= kEpsBytes || (d.grant > 0.0 && fadd(now, fdiv_exact(rem, d.grant)) <= now);
         if (!done) {
             reallocate_root(r);
             return;
@@ -621,7 +625,7 @@ struct Sim {
         d.remaining = 0.0;
         d.transferring = 0;
         const int k = d.tq_head - 1;
-        io.req_transfer_ms[d.base + k] = fadd(d.transfer_ms, fmul(fsub(st.now, d.started_s), 1000.0));
+        io.req_transfer_ms[d.base + k] = fadd(d.transfer_ms, fmul(fsub(now, d.started_s), 1000.0));
         rd[r].active &= ~(1ull << i);
         d.grant = 0.0;
         reallocate_root(r);
@@ -635,7 +639,7 @@ struct Sim {
         const int64_t base = d.base;
         const int k = d.cur_compute;
         const double arrived = io.arr_t[base + k];
-        double total = fmul(fsub(st.now, arrived), 1000.0);
+        double total = fmul(fsub(now, arrived), 1000.0);
         const double compute = fadd(d.compute_done_ms, d.svc_ms);
         const double transfer = d.cur_transfer_ms;
         double noise = fsub(fsub(total, compute), transfer);
@@ -643,7 +647,7 @@ struct Sim {
         total = fadd(fadd(compute, transfer), noise);
         const uint64_t idx = d.completed;
         d.completed += 1;
-        if (st.now >= S.measure_start_s) {
+        if (now >= S.measure_start_s) {
             io.win_lat[base + static_cast<int64_t>(d.n_window)] = total;
             d.n_window += 1;
             d.sum_total = fadd(d.sum_total, total);
@@ -653,7 +657,7 @@ struct Sim {
         }
         if (io.c_total) {
             const int64_t o = base + static_cast<int64_t>(idx);
-            io.c_done[o] = st.now;
+            io.c_done[o] = now;
             io.c_total[o] = total;
             io.c_compute[o] = compute;
             io.c_transfer[o] = transfer;
@@ -661,7 +665,7 @@ struct Sim {
         }
         start_compute(i);
         if (C.enabled) {
-            Action a = on_observation(i, total, st.now, arrived);
+            Action a = on_observation(i, total, now, arrived);
             if (a.valid) apply_action(a);
         }
     }
@@ -685,7 +689,7 @@ struct Sim {
                 if (in_last) io.backlog[2 * r + 1] = fadd(io.backlog[2 * r + 1], backlog);
             }
         }
-        const double nt = fadd(st.now, 1.0);
+        const double nt = fadd(now, 1.0);
         if (nt <= S.duration_s) push(kEvTick, 0, nt);
     }
 
@@ -711,13 +715,13 @@ struct Sim {
             d.grant = 0.0;
             cancel(kEvTransfer, i);
             if (d.started_s >= 0.0) {
-                d.transfer_ms = fadd(d.transfer_ms, fmul(fsub(st.now, d.started_s), 1000.0));
+                d.transfer_ms = fadd(d.transfer_ms, fmul(fsub(now, d.started_s), 1000.0));
                 d.started_s = -1.0;
             }
             reallocate_root(r);
         }
         if (d.computing) {
-            const double rm = fmul(fsub(d.compute_end, st.now), 1000.0);
+            const double rm = fmul(fsub(d.compute_end, now), 1000.0);
             const double remaining_ms = 0.0 < rm ? rm : 0.0;
             const double stage = fadd(d.svc_ms, d.extra_ms);
             const double frac = stage > 0.0 ? fdiv_exact(remaining_ms, stage) : 0.0;
@@ -728,10 +732,10 @@ struct Sim {
             cancel(kEvCompute, i);
         }
         d.paused = 1;
-        d.paused_until = fadd(st.now, duration);
+        d.paused_until = fadd(now, duration);
         if (st.n_pauses < io.pause_cap) {
             PauseRec& p = io.pauses[st.n_pauses];
-            p.t_s = st.now;
+            p.t_s = now;
             p.duration_s = duration;
             p.tenant = i;
             p.kind = cause_kind;
@@ -751,11 +755,11 @@ struct Sim {
         if (d.computing) {
             const double service = fdiv_exact(d.svc_ms, sm_fraction(i));
             d.svc_ms = service;
-            d.compute_end = fadd(st.now, fdiv_exact(fadd(service, d.extra_ms), 1000.0));
+            d.compute_end = fadd(now, fdiv_exact(fadd(service, d.extra_ms), 1000.0));
             push(kEvCompute, i, d.compute_end);
         }
         if (d.transferring) {
-            d.started_s = st.now;
+            d.started_s = now;
             const int r = root_of(i);
             settle_root(r);
             rd[r].active |= 1ull << i;
@@ -765,7 +769,7 @@ struct Sim {
         start_compute(i);
         if (d.has_pend) {
             d.has_pend = 0;
-            on_action_applied(i, d.pend_kind, st.now, d.pend_pause);
+            on_action_applied(i, d.pend_kind, now, d.pend_pause);
         }
     }
 
@@ -795,7 +799,7 @@ struct Sim {
             rec->target = i;
             rec->diagnosis = kDiagNone;
             rec->expire_kind = kind;
-            rec->t_s = st.now;
+            rec->t_s = now;
         }
     }
 
@@ -812,13 +816,13 @@ struct Sim {
                     settle_root(r);
                     reallocate_root(r);
                 }
-                on_action_applied(a.tenant, a.kind, st.now, 0.0);
+                on_action_applied(a.tenant, a.kind, now, 0.0);
                 break;
             }
             case kActMpsQuota: {
                 tgt.mps_quota = a.quota_pct;
                 push(kEvExpire, a.target, a.expires_at_s);
-                on_action_applied(a.tenant, a.kind, st.now, 0.0);
+                on_action_applied(a.tenant, a.kind, now, 0.0);
                 break;
             }
             case kActMove: {
@@ -857,7 +861,7 @@ struct Sim {
                         settle_root(r);
                         reallocate_root(r);
                     }
-                    on_action_applied(a.tenant, a.kind, st.now, 0.0);
+                    on_action_applied(a.tenant, a.kind, now, 0.0);
                     break;
                 }
                 TenantDyn& d = td[a.tenant];
@@ -1052,7 +1056,7 @@ struct Sim {
             a.target = off;
             a.diagnosis = diag;
             a.throttle_Bps = C.guardrail_io_throttle_Bps;
-            a.expires_at_s = fadd(st.now, C.throttle_duration_s);
+            a.expires_at_s = fadd(now, C.throttle_duration_s);
             return a;
         }
         if (diag == kDiagCompute) {
@@ -1077,7 +1081,7 @@ struct Sim {
             a.target = off;
             a.diagnosis = diag;
             a.quota_pct = C.guardrail_mps_quota_pct;
-            a.expires_at_s = fadd(st.now, C.quota_duration_s);
+            a.expires_at_s = fadd(now, C.quota_duration_s);
             return a;
         }
         return a;
@@ -1199,7 +1203,7 @@ struct Sim {
             n.tenant = i;
             n.target = i;
             n.diagnosis = diag;
-            record(n, st.now, c);
+            record(n, now, c);
             c.none_logged = 1;
         }
         c.next_rung = 0;
@@ -1353,21 +1357,16 @@ struct Sim {
 
     // ---- setup and main loop (engine.cpp:239-277, 864-894) -------------------------------
     MG_HD void init(const int32_t* file_order, double* win_storage, double* vwin_storage) {
-        st.now = 0.0;
-        st.next_seq = 0;
+        now = 0.0;
+        next_seq = n_events = live_resume = live_expire = 0;
         st.n_actions = st.n_pauses = st.error = st.next_action_seq = 0;
-        st.n_events = 0;
-        st.n_rare = 0;
-        st.tick_index = 0;
+        st.tick_index = st.pad = 0;
         for (int r = 0; r < S.n_roots; ++r) {
             rd[r].active = 0;
             io.backlog[2 * r] = 0.0;
             io.backlog[2 * r + 1] = 0.0;
         }
-        for (int s = 0; s <= kEvKinds * T; ++s) {
-            slots[s].t = k_inf();
-            slots[s].key = ~0ull;
-        }
+        for (int s = 0; s <= kEvKinds * T; ++s) lanes.clear(s);
         for (int i = 0; i < T; ++i) {
             const PTenant& p = spec(i);
             TenantDyn& d = td[i];
@@ -1420,19 +1419,14 @@ struct Sim {
         push(kEvTick, 0, 1.0);
     }
 
-    // true if slot s holds the next event to run (engine.cpp:869-872)
-    MG_HD bool runnable(int s) const { return slots[s].key != ~0ull && !(slots[s].t > S.duration_s); }
+    // tenant of slot s holding an event of `kind`
+    MG_HD int slot_tenant(int kind, int s) const { return kind == kEvTick ? 0 : s - slot_base(kind); }
 
-    // pop slot s and dispatch its event (engine.cpp:873-881)
-    MG_HD void dispatch(int s) {
-        const double t = slots[s].t;
-        const int kind = static_cast<int>(slots[s].key >> 48);
-        const int i = kind == kEvTick ? 0 : s - slot_base(kind);
-        if (rare_kind(kind)) st.n_rare -= 1;
-        slots[s].t = k_inf();
-        slots[s].key = ~0ull;
-        st.now = t;
-        st.n_events += 1;
+    // run the popped event (its slot already cleared by the caller) (engine.cpp:873-881)
+    MG_HD void dispatch(int kind, int i, double t) {
+        if (rare_kind(kind)) mark_rare(kind, i, false);
+        now = t;
+        n_events += 1;
         switch (kind) {
             case kEvResume: on_resume(i); break;
             case kEvExpire: on_guardrail_expire(i); break;
@@ -1443,14 +1437,18 @@ struct Sim {
         }
     }
 
+    // host event loop (engine.cpp:864-894); the device loop lives in des_kernel
     MG_HD void run() {
         const int nslots = kEvKinds * T + 1;
         for (;;) {
-            const int s = lanes.argmin_slot(slots, nslots);
-            if (!runnable(s)) break;
-            dispatch(s);
+            const int s = lanes.argmin(nslots);
+            const Slot e = lanes.slots[s];
+            if (e.key == ~0ull || e.t > S.duration_s) break;  // engine.cpp:869-872
+            lanes.clear(s);
+            const int kind = static_cast<int>(e.key >> 48);
+            dispatch(kind, slot_tenant(kind, s), e.t);
         }
-        st.now = S.duration_s;
+        now = S.duration_s;
     }
 
     MG_HD void finish() {
@@ -1473,18 +1471,29 @@ struct Sim {
         io.rout->n_actions = st.n_actions;
         io.rout->n_pauses = st.n_pauses;
         // the device event order packs seq into 29 bits (engine_kernels.cu); never silently wrap
-        io.rout->error = st.next_seq >= (1ull << 29) ? kErrSeqOverflow : st.error;
+        io.rout->error = next_seq >= (1ull << 29) ? kErrSeqOverflow : st.error;
         io.rout->pad = 0;
-        io.rout->n_events = st.n_events;
+        io.rout->n_events = n_events;
     }
 };
 
-// Host "warp": one lane, linear argmin.
+// Event slots in memory with a linear argmin: the host harness (one lane) and the device
+// fallback for tenant counts too large for lane-register slots (des_kernel scans them).
 struct HostLanes {
-    MG_HD int argmin_slot(const Slot* s, int n) const {
+    Slot* slots;  // 5T + 1
+    MG_HD void set(int s, double t, uint64_t key) {
+        slots[s].t = t;
+        slots[s].key = key;
+    }
+    MG_HD void clear(int s) {
+        slots[s].t = k_inf();
+        slots[s].key = ~0ull;
+    }
+    MG_HD int argmin(int n) const {
         int best = 0;
         for (int k = 1; k < n; ++k)
-            if (s[k].t < s[best].t || (s[k].t == s[best].t && s[k].key < s[best].key)) best = k;
+            if (slots[k].t < slots[best].t || (slots[k].t == slots[best].t && slots[k].key < slots[best].key))
+                best = k;
         return best;
     }
 };

@@ -253,7 +253,8 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         B.prof = prof.p;
     }
 
-    CK(cudaFuncSetAttribute(mg::des_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+    auto* des = T <= mg::kRegSlotMaxTenants ? mg::des_kernel_reg : mg::des_kernel;
+    CK(cudaFuncSetAttribute(des, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
     const size_t sel_smem = mg::select_smem_bytes();
     CK(cudaFuncSetAttribute(mg::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sel_smem)));
 
@@ -287,7 +288,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         mg::gen_marks_kernel<<<static_cast<unsigned>(4 * nt), 32, 0, s>>>(A.scen.p, B, w);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[1], s));
-        mg::des_kernel<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
+        des<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[2], s));
         mg::select_kernel<<<static_cast<unsigned>(nt), 256, sel_smem, s>>>(B, T, w);

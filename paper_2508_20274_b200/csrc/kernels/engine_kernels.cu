@@ -56,8 +56,131 @@ size_t gen_times_smem_bytes() { return sizeof(GammaSmem); }
 
 // ---------------------------------------------------------------------------------------------
 // replica DES: one warp per replica, working set in dynamic shared memory
-__global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C,
-                                                 WaveBuffers B, int n_rep, SimLayout L) {
+//
+// Event order.  Event times are >= 0, so the IEEE bit pattern orders them as unsigned integers;
+// the total order (t, kind, seq) (engine.cpp:69-75) becomes (t_hi, t_lo, kind<<29 | seq) and the
+// warp minimum is one to three redux.sync.min.u32 steps.  seq < 2^29 per replica is checked by
+// Sim::finish.
+__device__ __forceinline__ uint32_t order_q(uint64_t key) {
+    return static_cast<uint32_t>((key >> 48) << 29) | static_cast<uint32_t>(key & 0x1fffffffu);
+}
+
+// Event slots as lane registers (T <= kRegSlotMaxTenants): lane k owns hot slot k (< 3T+1:
+// compute, transfer, arrival, tick) and rare slot k (< 2T: resume, expire).  A push is a
+// predicated register write in the owning lane; the argmin reads no memory.
+struct RegLanes {
+    int lane, nhot;
+    uint32_t hh, hl, hq;  // hot slot (t_hi, t_lo, q); hh == ~0 when empty
+    uint32_t rh, rl, rq;  // rare slot
+    __device__ __forceinline__ void put(int s, uint32_t h, uint32_t l, uint32_t q) {
+        if (s < nhot) {
+            if (lane == s) {
+                hh = h;
+                hl = l;
+                hq = q;
+            }
+        } else if (lane == s - nhot) {
+            rh = h;
+            rl = l;
+            rq = q;
+        }
+    }
+    __device__ __forceinline__ void set(int s, double t, uint64_t key) {
+        const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(t));
+        put(s, static_cast<uint32_t>(tb >> 32), static_cast<uint32_t>(tb), order_q(key));
+    }
+    __device__ __forceinline__ void clear(int s) { put(s, 0xffffffffu, 0xffffffffu, 0xffffffffu); }
+};
+
+template <class Lanes>
+__device__ __forceinline__ Lanes make_lanes(unsigned char* smem, const SimLayout& L, int T);
+template <>
+__device__ __forceinline__ HostLanes make_lanes<HostLanes>(unsigned char* smem, const SimLayout& L, int) {
+    return HostLanes{reinterpret_cast<Slot*>(smem + L.slots)};
+}
+template <>
+__device__ __forceinline__ RegLanes make_lanes<RegLanes>(unsigned char*, const SimLayout&, int T) {
+    RegLanes r;
+    r.lane = static_cast<int>(threadIdx.x);
+    r.nhot = 3 * T + 1;
+    r.hh = r.hl = r.hq = r.rh = r.rl = r.rq = 0xffffffffu;
+    return r;
+}
+
+// Warp argmin of the next event.  Returns false when no live event is left.  On success every
+// lane holds the winner's slot index and (t, q).
+template <class Lanes>
+__device__ __forceinline__ bool next_event(Sim<Lanes>& sim, int T, int& s_out, double& t_out, uint32_t& q_out);
+
+template <>
+__device__ __forceinline__ bool next_event<RegLanes>(Sim<RegLanes>& sim, int, int& s_out, double& t_out,
+                                                     uint32_t& q_out) {
+    RegLanes& R = sim.lanes;
+    uint32_t h = R.hh, l = R.hl, q = R.hq;
+    int s = R.lane;
+    if (sim.any_rare() && (R.rh < h || (R.rh == h && (R.rl < l || (R.rl == l && R.rq < q))))) {
+        h = R.rh;
+        l = R.rl;
+        q = R.rq;
+        s = R.nhot + R.lane;
+    }
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, h);
+    if (m1 == 0xffffffffu) return false;  // no live event (every t >= 0 has a smaller high word)
+    unsigned win = __ballot_sync(0xffffffffu, h == m1);
+    if (win & (win - 1)) {  // equal high words: low words decide, then (kind, seq)
+        const uint32_t m2 = __reduce_min_sync(0xffffffffu, h == m1 ? l : 0xffffffffu);
+        win = __ballot_sync(0xffffffffu, h == m1 && l == m2);
+        if (win & (win - 1)) {
+            const uint32_t m3 = __reduce_min_sync(0xffffffffu, (h == m1 && l == m2) ? q : 0xffffffffu);
+            win = __ballot_sync(0xffffffffu, h == m1 && l == m2 && q == m3);
+        }
+    }
+    const int wl = __ffs(win) - 1;
+    const uint32_t lo = __shfl_sync(0xffffffffu, l, wl);
+    q_out = __shfl_sync(0xffffffffu, q, wl);
+    s_out = __shfl_sync(0xffffffffu, s, wl);
+    t_out = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | lo));
+    return true;
+}
+
+template <>
+__device__ __forceinline__ bool next_event<HostLanes>(Sim<HostLanes>& sim, int T, int& s_out, double& t_out,
+                                                      uint32_t& q_out) {
+    const Slot* slots = sim.lanes.slots;
+    const int lane = threadIdx.x;
+    uint32_t hi = 0xffffffffu, lo = 0xffffffffu, kq = 0xffffffffu;
+    int bi = -1;
+    const int nslots = sim.any_rare() ? kEvKinds * T + 1 : 3 * T + 1;
+    for (int k = lane; k < nslots; k += 32) {
+        const uint64_t key = slots[k].key;
+        if (key == ~0ull) continue;
+        const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(slots[k].t));
+        const uint32_t h = static_cast<uint32_t>(tb >> 32), l = static_cast<uint32_t>(tb), q = order_q(key);
+        if (h < hi || (h == hi && (l < lo || (l == lo && q < kq)))) {
+            hi = h;
+            lo = l;
+            kq = q;
+            bi = k;
+        }
+    }
+    const uint32_t m1 = __reduce_min_sync(0xffffffffu, hi);
+    if (m1 == 0xffffffffu) return false;
+    const uint32_t m2 = __reduce_min_sync(0xffffffffu, hi == m1 ? lo : 0xffffffffu);
+    unsigned win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2);
+    if (win & (win - 1)) {  // equal times: (kind, seq) decides
+        const uint32_t m3 = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? kq : 0xffffffffu);
+        win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2 && kq == m3);
+    }
+    const int wl = __ffs(win) - 1;
+    s_out = __shfl_sync(0xffffffffu, bi, wl);
+    q_out = __shfl_sync(0xffffffffu, kq, wl);
+    t_out = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | m2));
+    return true;
+}
+
+template <class Lanes>
+__device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const PController* __restrict__ C,
+                                         const WaveBuffers& B, int n_rep, const SimLayout& L) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int r = blockIdx.x;
     if (r >= n_rep) return;
@@ -81,7 +204,6 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     TenantDyn* td = reinterpret_cast<TenantDyn*>(smem + L.td);
     TenantCtl* ctl = reinterpret_cast<TenantCtl*>(smem + L.ctl);
     RootDyn* rd = reinterpret_cast<RootDyn*>(smem + L.rd);
-    Slot* slots = reinterpret_cast<Slot*>(smem + L.slots);
     double* win;
     double* vwin;
     if (B.rings_in_smem) {
@@ -120,7 +242,7 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     } else {
         io.c_done = io.c_total = io.c_compute = io.c_transfer = io.c_noise = nullptr;
     }
-    Sim<HostLanes> sim(*S, Cv, io, st, slots, HostLanes{}, td, ctl, rd);
+    Sim<Lanes> sim(*S, Cv, io, st, make_lanes<Lanes>(smem, L, T), td, ctl, rd);
     sim.tn = reinterpret_cast<const PTenant*>(smem + L.sc_tn);
     sim.gp = reinterpret_cast<const PGpu*>(smem + L.sc_gp);
     sim.rt = reinterpret_cast<const PRoot*>(smem + L.sc_rt);
@@ -131,12 +253,7 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     // (BSSY/BSYNC) wraps the hot path.
     sim.init(B.file_order, win, vwin);
     __syncwarp();
-    // Event loop: the warp finds the next event (argmin over the 5T+1 event slots, lane-parallel
-    // with a butterfly reduction), lane 0 runs the handler on the shared-memory state.
-    // Event times are >= 0, so the IEEE bit pattern orders them as unsigned integers; the total
-    // order (t, kind, seq) (engine.cpp:69-75) becomes (t_hi, t_lo, kind<<29 | seq) and the warp
-    // minimum is three redux.sync.min.u32 steps.  seq < 2^29 per replica is checked by the host.
-    const int nslots_all = kEvKinds * T + 1, nslots_hot = 3 * T + 1;
+    const double duration = S->duration_s;
 #ifdef MG_PROFILE_EVENTS
     // build-time instrumentation (make PROFILE=1): SM cycles spent choosing vs running events
     unsigned long long c_pick[6] = {0, 0, 0, 0, 0, 0}, c_run[6] = {0, 0, 0, 0, 0, 0}, n_ev[6] = {0, 0, 0, 0, 0, 0};
@@ -145,38 +262,17 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
 #ifdef MG_PROFILE_EVENTS
         const long long c0 = clock64();
 #endif
-        uint32_t hi = 0xffffffffu, lo = 0xffffffffu, kq = 0xffffffffu;
-        int bi = -1;
-        const int nslots = st.n_rare ? nslots_all : nslots_hot;
-        for (int k = lane; k < nslots; k += 32) {
-            const uint64_t key = slots[k].key;
-            if (key == ~0ull) continue;
-            const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(slots[k].t));
-            const uint32_t h = static_cast<uint32_t>(tb >> 32), l = static_cast<uint32_t>(tb);
-            const uint32_t q = static_cast<uint32_t>((key >> 48) << 29) | static_cast<uint32_t>(key & 0x1fffffffu);
-            if (h < hi || (h == hi && (l < lo || (l == lo && q < kq)))) {
-                hi = h;
-                lo = l;
-                kq = q;
-                bi = k;
-            }
-        }
-        const uint32_t m1 = __reduce_min_sync(0xffffffffu, hi);
-        if (m1 == 0xffffffffu) break;  // no live event (every t >= 0 has a smaller high word)
-        const uint32_t m2 = __reduce_min_sync(0xffffffffu, hi == m1 ? lo : 0xffffffffu);
-        unsigned win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2);
-        if (win & (win - 1)) {  // equal times: (kind, seq) decides
-            const uint32_t m3 = __reduce_min_sync(0xffffffffu, (hi == m1 && lo == m2) ? kq : 0xffffffffu);
-            win = __ballot_sync(0xffffffffu, bi >= 0 && hi == m1 && lo == m2 && kq == m3);
-        }
-        const int s = __shfl_sync(0xffffffffu, bi, __ffs(win) - 1);
-        const double t = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(m1) << 32) | m2));
-        if (t > S->duration_s) break;
+        int s;
+        double t;
+        uint32_t q;
+        if (!next_event(sim, T, s, t, q)) break;
+        if (t > duration) break;  // engine.cpp:872
+        const int kind = static_cast<int>(q >> 29);
+        sim.lanes.clear(s);
 #ifdef MG_PROFILE_EVENTS
-        const int kind = static_cast<int>(slots[s].key >> 48);
         const long long c1 = clock64();
 #endif
-        sim.dispatch(s);
+        sim.dispatch(kind, sim.slot_tenant(kind, s), t);
         __syncwarp();
 #ifdef MG_PROFILE_EVENTS
         const long long c2 = clock64();
@@ -185,7 +281,7 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
         n_ev[kind] += 1;
 #endif
     }
-    st.now = S->duration_s;
+    sim.now = duration;
     sim.finish();
 #ifdef MG_PROFILE_EVENTS
     if (lane == 0 && B.prof)
@@ -197,6 +293,16 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
 #endif
 }
 
+__global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C,
+                                                 WaveBuffers B, int n_rep, SimLayout L) {
+    des_body<HostLanes>(S, C, B, n_rep, L);
+}
+
+__global__ void __launch_bounds__(32) des_kernel_reg(const PScenario* __restrict__ S,
+                                                     const PController* __restrict__ C, WaveBuffers B, int n_rep,
+                                                     SimLayout L) {
+    des_body<RegLanes>(S, C, B, n_rep, L);
+}
 
 // ---------------------------------------------------------------------------------------------
 __global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,

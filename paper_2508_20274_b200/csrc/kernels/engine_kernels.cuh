@@ -48,6 +48,10 @@ __global__ void gen_times_kernel(const PScenario* __restrict__ S, WaveBuffers B,
 __global__ void gen_marks_kernel(const PScenario* __restrict__ S, WaveBuffers B, int n_rep);
 __global__ void des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
                            int n_rep, SimLayout L);
+// same, with the event slots in lane registers; for T <= kRegSlotMaxTenants
+constexpr int kRegSlotMaxTenants = 10;  // 3T+1 hot slots and 2T rare slots within 32 lanes
+__global__ void des_kernel_reg(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
+                               int n_rep, SimLayout L);
 __global__ void select_kernel(WaveBuffers B, int T, int n_rep);
 __global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
                                        const int64_t* __restrict__ dst_off, ActionRec* __restrict__ dst, int n_rep);

@@ -143,7 +143,7 @@ char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, in
             io.c_transfer = ctr.data();
             io.c_noise = cn.data();
         }
-        mg::Sim<mg::HostLanes> sim(P.scen, C, io, st, slots, mg::HostLanes{}, st.td, st.ctl, st.rd);
+        mg::Sim<mg::HostLanes> sim(P.scen, C, io, st, mg::HostLanes{slots}, st.td, st.ctl, st.rd);
         sim.init(P.file_order.data(), reinterpret_cast<double*>(base + L.win), reinterpret_cast<double*>(base + L.vwin));
         sim.run();
         sim.finish();

@@ -57,6 +57,8 @@ typedef struct migsim_run_opts {
     int32_t max_wave_replicas;  /* 0: sized from free device memory */
     int32_t action_cap;         /* per-replica action-log capacity, 0: default 1024 */
     int32_t pause_cap;          /* per-replica pause-log capacity, 0: default 1024 */
+    int32_t write_traces;       /* RunOptions::write_traces: per-completion + per-tick trace rows
+                                   (requests/counters/fabric streams, engine.cpp:279-288) */
 } migsim_run_opts;
 
 /* device-side timing of the last batch (CUDA events on the batch stream), milliseconds */
@@ -88,6 +90,14 @@ MIGSIM_API int migsim_scenario_tenant_id(migsim_gpu* g, int32_t scenario_id, int
 MIGSIM_API int migsim_gpu_run_batch(migsim_gpu* g, int32_t scenario_id, const migsim_variant* variants, size_t n_variants,
                          const uint64_t* seeds, size_t n_seeds, const migsim_run_opts* opts,
                          migsim_batch_result** out, char* err, size_t errlen);
+
+/* engine::run_scenario(spec, RunOptions{seed, out_dir, write_traces}) (engine.hpp:94-99,117): one
+ * replica on the GPU; the host writes the reference's artifacts into out_dir byte-for-byte
+ * (summary.json, actions.jsonl and, with write_traces, requests.csv / counters.csv / fabric.csv;
+ * engine.cpp:279-288,889-892, trace.cpp).  *result_json (optional, free with migsim_free) receives
+ * the RunResult as JSON. */
+MIGSIM_API int migsim_gpu_run_scenario(migsim_gpu* g, int32_t scenario_id, const migsim_variant* variant, uint64_t seed,
+                            const char* out_dir, int32_t write_traces, char** result_json, char* err, size_t errlen);
 
 MIGSIM_API size_t migsim_batch_n_runs(const migsim_batch_result* r);
 MIGSIM_API int migsim_batch_n_tenants(const migsim_batch_result* r);

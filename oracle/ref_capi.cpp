@@ -239,6 +239,26 @@ void* ref_run(const char* scenario_json, const char* overrides_json, uint64_t se
     }
 }
 
+// engine::run_scenario with files: RunOptions{seed, out_dir, write_traces} -- the reference's own
+// trace/summary/actions writers (engine.cpp:279-288, 889-892; trace.cpp).  Returns 0 on success.
+int ref_run_artifacts(const char* scenario_json, const char* overrides_json, uint64_t seed, const char* out_dir,
+                      int write_traces) {
+    try {
+        auto spec = scenario::parse_scenario(scenario_json, "<scenario>");
+        apply_overrides(spec, overrides_json);
+        engine::RunOptions ro;
+        ro.seed = seed;
+        ro.out_dir = out_dir;
+        ro.write_traces = write_traces != 0;
+        ro.keep_completions = false;
+        (void)engine::run_scenario(spec, ro);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 const char* ref_result_json(void* hp) { return static_cast<Handle*>(hp)->json_text.c_str(); }
 
 size_t ref_result_n_completions(void* hp) { return static_cast<Handle*>(hp)->result.completions.size(); }

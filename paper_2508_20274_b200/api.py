@@ -52,6 +52,7 @@ class _RunOpts(ctypes.Structure):
         ("max_wave_replicas", ctypes.c_int32),
         ("action_cap", ctypes.c_int32),
         ("pause_cap", ctypes.c_int32),
+        ("write_traces", ctypes.c_int32),
     ]
 
 
@@ -146,6 +147,8 @@ def load_library() -> ctypes.CDLL:
         vp, ctypes.c_void_p, ctypes.c_void_p, sz, ctypes.c_void_p, sz, ctypes.c_void_p,
         ctypes.POINTER(ctypes.c_double), cp, sz,
     ]
+    lib.migsim_gpu_run_scenario.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(_Variant), ctypes.c_uint64, cp,
+                                            ctypes.c_int32, ctypes.POINTER(vp), cp, sz]
     lib.migsim_run_plan.argtypes = [vp, cp, cp, ctypes.c_int32, ctypes.c_uint64, cp, ctypes.POINTER(vp), cp, sz]
     lib.migsim_free.argtypes = [vp]
     _lib_handle = lib
@@ -298,7 +301,7 @@ class Engine:
         variants = list(variants) if variants else [Variant()]
         cv = (_Variant * len(variants))(*[v._c() for v in variants])
         cs = (ctypes.c_uint64 * len(seeds))(*[int(s) for s in seeds])
-        opts = _RunOpts(int(keep_completions), int(max_wave_replicas), 0, 0)
+        opts = _RunOpts(int(keep_completions), int(max_wave_replicas), 0, 0, 0)
         out = ctypes.c_void_p()
         err = ctypes.create_string_buffer(2048)
         _check(self._lib.migsim_gpu_run_batch(self._h, sid, cv, len(variants), cs, len(seeds), ctypes.byref(opts),
@@ -312,6 +315,22 @@ class Engine:
         timing = {k: getattr(t, k) for k, _ in _Timing._fields_}
         return BatchResult(n_runs, T, self.tenant_ids(sid), variants, [int(s) for s in seeds],
                            rows.reshape(n_runs, T), timing, out.value, self)
+
+    def run_scenario(self, sid: int, seed: int = 1, variant: Optional[Variant] = None, out_dir: str = "",
+                     write_traces: bool = True) -> dict:
+        """engine::run_scenario(spec, RunOptions{seed, out_dir, write_traces}) (engine.hpp:94-99,117):
+        one replica on the GPU; with out_dir the reference's artifacts are written there byte-for-byte
+        (summary.json, actions.jsonl, and requests/counters/fabric.csv when write_traces)."""
+        cv = variant._c() if variant else None
+        out = ctypes.c_void_p()
+        err = ctypes.create_string_buffer(2048)
+        _check(self._lib.migsim_gpu_run_scenario(self._h, sid, ctypes.byref(cv) if cv else None, int(seed),
+                                                 out_dir.encode() if out_dir else None, int(write_traces),
+                                                 ctypes.byref(out), err, 2048), err)
+        try:
+            return json.loads(ctypes.string_at(out.value).decode())
+        finally:
+            self._lib.migsim_free(out)
 
     def select(self, segments: Sequence[np.ndarray], qs: Sequence[float]) -> (np.ndarray, float):
         """Nearest-rank quantiles of each segment on the GPU; returns (out[n_seg, n_q], device_ms)."""
@@ -350,10 +369,13 @@ def default_engine() -> Engine:
 
 
 def run_scenario(scenario_path: str, seed: int = 1, variant: Optional[Variant] = None,
-                 keep_completions: bool = False) -> dict:
-    """engine::run_scenario as a 1x1 batch on the GPU (engine.hpp:117)."""
+                 keep_completions: bool = False, out_dir: str = "", write_traces: bool = True) -> dict:
+    """engine::run_scenario as a 1x1 batch on the GPU (engine.hpp:117).  With out_dir, the run's
+    artifacts are written like RunOptions{seed, out_dir, write_traces} (engine.cpp:279-288,889-892)."""
     eng = default_engine()
     sid = eng.load_scenario(scenario_path)
+    if out_dir:
+        return eng.run_scenario(sid, seed, variant, out_dir, write_traces)
     res = eng.run_batch(sid, [seed], [variant] if variant else None, keep_completions=keep_completions)
     out = res.run(0)
     if keep_completions:

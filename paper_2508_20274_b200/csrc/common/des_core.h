@@ -42,6 +42,8 @@ enum EvKind : int32_t { kEvResume = 0, kEvExpire = 1, kEvTransfer = 2, kEvComput
 constexpr double kEpsBytes = 1e-6;   // engine.cpp:48
 constexpr double kMpsKappa = 0.5;    // engine.hpp:42
 
+struct TailWin;
+
 // ---------------------------------------------------------------------------------------------
 // per-replica inputs/outputs in global memory
 struct ReplicaIO {
@@ -72,6 +74,12 @@ struct ReplicaIO {
     double* c_compute;
     double* c_transfer;
     double* c_noise;
+    int64_t* c_order;  // position of the completion in the replica's completion sequence
+    // optional per-tick traces (write_traces): rows [n_ticks][T] / [n_ticks][R], and the per-tenant
+    // 256-sample trace window (engine.cpp:115, pushed on every completion, :497)
+    CounterRow* tr_cnt;
+    FabricRow* tr_fab;
+    TailWin* tr_win;
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -237,6 +245,14 @@ struct TenantDyn {
     double cap_eff; // effective_pcie_cap_Bps of the current throttle state (model.cpp:155-159)
 };
 
+MG_HD int __popcll_hd(uint64_t m) {
+#if defined(__CUDA_ARCH__)
+    return __popcll(static_cast<unsigned long long>(m));
+#else
+    return __builtin_popcountll(m);
+#endif
+}
+
 MG_HD void prefetch_l1(const void* p) {
 #if defined(__CUDA_ARCH__)
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -260,6 +276,7 @@ struct Slot {
 struct SimState {
     int32_t n_actions, n_pauses, error, next_action_seq;
     int32_t tick_index, pad;
+    int64_t done_seq;  // completions so far (order of the requests.csv stream)
     TenantDyn* td;   // n_tenants
     TenantCtl* ctl;  // n_tenants
     RootDyn* rd;     // n_roots
@@ -662,7 +679,10 @@ struct Sim {
             io.c_compute[o] = compute;
             io.c_transfer[o] = transfer;
             io.c_noise[o] = noise;
+            if (io.c_order) io.c_order[o] = st.done_seq;
         }
+        st.done_seq += 1;
+        if (io.tr_win) tw_push(io.tr_win[i], total);
         start_compute(i);
         if (C.enabled) {
             Action a = on_observation(i, total, now, arrived);
@@ -670,9 +690,40 @@ struct Sim {
         }
     }
 
+    // counters.csv / fabric.csv rows of tick j (engine.cpp:746-775)
+    MG_HD void trace_tick(int j) {
+        for (int r = 0; r < S.n_roots; ++r) {
+            double backlog = 0.0;
+            for (int i = 0; i < T; ++i) {
+                const TenantDyn& d = td[i];
+                if (d.host != rt[r].host || root_of(i) != r) continue;
+                if (d.transferring) backlog = fadd(backlog, d.remaining);
+                for (int k = d.tq_head; k < d.n_arrived; ++k) backlog = fadd(backlog, io.arr_bytes[d.base + k]);
+            }
+            FabricRow& f = io.tr_fab[static_cast<int64_t>(j) * S.n_roots + r];
+            f.offered_Bps = root_offered(r);
+            f.backlog_bytes = backlog;
+            f.active_flows = __popcll_hd(rd[r].active);
+            f.pad = 0;
+        }
+        for (int i = 0; i < T; ++i) {
+            const TenantDyn& d = td[i];
+            CounterRow& c = io.tr_cnt[static_cast<int64_t>(j) * T + i];
+            c.completed = d.completed;
+            c.queue_len = queue_len(i);
+            c.window_p99_ms = io.tr_win[i].n > 0 ? tw_quantile(io.tr_win[i], 0.99) : 0.0;
+            c.grant_Bps = d.transferring ? d.grant : 0.0;
+            c.profile = d.profile;
+            c.host = d.host;
+            c.gpu_id = gp[d.gpu].id;
+            c.pad = 0;
+        }
+    }
+
     MG_HD void on_tick() {
         const int third = S.n_ticks / 3;
         const int j = st.tick_index++;
+        if (io.tr_cnt) trace_tick(j);
         if (S.n_ticks >= 10 && third > 0) {
             for (int r = 0; r < S.n_roots; ++r) {
                 const bool in_first = j < third, in_last = j >= S.n_ticks - third;
@@ -1361,6 +1412,7 @@ struct Sim {
         next_seq = n_events = live_resume = live_expire = 0;
         st.n_actions = st.n_pauses = st.error = st.next_action_seq = 0;
         st.tick_index = st.pad = 0;
+        st.done_seq = 0;
         for (int r = 0; r < S.n_roots; ++r) {
             rd[r].active = 0;
             io.backlog[2 * r] = 0.0;
@@ -1411,6 +1463,7 @@ struct Sim {
             c.window_end_s = C.sample_interval_s;
             c.ignore_before_s = c.validation_start_s = c.pre_p99_ms = c.ema = 0.0;
             c.app_kind = c.app_target = c.app_diag = 0;
+            if (io.tr_win) tw_reset(io.tr_win[i], k_inf());
         }
         for (int n = 0; n < T; ++n) {
             const int i = file_order[n];

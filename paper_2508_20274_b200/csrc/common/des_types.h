@@ -48,6 +48,19 @@ struct TenantOut {
     double win_min, win_max;  // range of the measurement-window latencies (seeds the radix select)
 };
 
+// Per-tick trace rows (engine.cpp:744-775 with RunOptions::write_traces; formatted on the host by
+// the trace.cpp equivalents).  counters.csv: one row per (tick, tenant in id order);
+// fabric.csv: one row per (tick, root in (host, id) order).
+struct CounterRow {
+    uint64_t completed, queue_len;
+    double window_p99_ms, grant_Bps;
+    int32_t profile, host, gpu_id, pad;
+};
+struct FabricRow {
+    double offered_Bps, backlog_bytes;
+    int32_t active_flows, pad;
+};
+
 // error codes (C-ABI return codes, include/migsim_b200.h)
 enum : int32_t {
     kErrNone = 0,

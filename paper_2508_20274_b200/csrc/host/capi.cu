@@ -16,6 +16,7 @@
 
 #include "../../../include/migsim_b200.h"
 #include "../kernels/engine_kernels.cuh"
+#include "artifacts.hpp"
 #include "packer.hpp"
 #include "result_json.hpp"
 
@@ -107,6 +108,7 @@ struct migsim_batch_result {
     std::vector<double> comps;
     std::vector<int64_t> comp_off;
     std::vector<std::string> json;
+    std::vector<mgb::TraceRows> traces;  // per run, with write_traces
     migsim_timing timing{};
 };
 
@@ -115,14 +117,18 @@ namespace {
 struct WaveAlloc {
     DevBuf<double> arr_t, arr_bytes, arr_mult, arr_noise, irq_e, t_all, req_ms, win_lat;
     DevBuf<double> c_done, c_total, c_compute, c_transfer, c_noise;
-    DevBuf<int32_t> n_all, n_kept, variant, gen_overflow, file_order;
+    DevBuf<int32_t> n_all, n_kept, variant, gen_overflow, file_order, sel_order;
     DevBuf<uint64_t> mt_pause, seeds;
     DevBuf<mg::ActionRec> actions, actions_c;
     DevBuf<mg::PauseRec> pauses, pauses_c;
     DevBuf<mg::TenantOut> tout;
     DevBuf<mg::ReplicaOut> rout;
     DevBuf<double> backlog, quant, rings;
-    DevBuf<int64_t> off, cap, act_off, pause_off;
+    DevBuf<int64_t> off, cap, act_off, pause_off, c_order;
+    DevBuf<mg::CounterRow> tr_cnt;
+    DevBuf<mg::FabricRow> tr_fab;
+    DevBuf<mg::TailWin> tr_win;
+    DevBuf<double> tr_ring;
     DevBuf<mg::PScenario> scen;
     DevBuf<mg::PController> ctrl;
 };
@@ -143,7 +149,8 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.n_runs = n_jobs;
     res.T = T;
     res.R = R;
-    const bool keep = opts.keep_completions != 0;
+    const bool traces = opts.write_traces != 0;
+    const bool keep = opts.keep_completions != 0 || traces;
     // working-set layout: controller rings in shared memory when a replica stays under 96 KB
     const int G = P.scen.n_gpus, I = P.scen.n_irq, H = P.scen.n_hosts;
     mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true, G, I, H);
@@ -178,6 +185,23 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         A.c_compute.alloc(big);
         A.c_transfer.alloc(big);
         A.c_noise.alloc(big);
+        A.c_order.alloc(big);
+    }
+    const int n_ticks = P.scen.n_ticks;
+    constexpr int kTraceWin = 256;  // engine.cpp:115
+    if (traces) {
+        A.tr_cnt.alloc(W * static_cast<size_t>(n_ticks) * T);
+        A.tr_fab.alloc(W * static_cast<size_t>(n_ticks) * R);
+        A.tr_win.alloc(W * T);
+        A.tr_ring.alloc(W * T * kTraceWin);
+        std::vector<mg::TailWin> tw(W * T);
+        for (size_t k = 0; k < W * T; ++k) {
+            std::memset(&tw[k], 0, sizeof(mg::TailWin));
+            tw[k].ring = A.tr_ring.p + k * kTraceWin;
+            tw[k].cap = kTraceWin;
+        }
+        CK(cudaMemcpy(A.tr_win.p, tw.data(), sizeof(mg::TailWin) * W * T, cudaMemcpyHostToDevice));
+        res.traces.resize(n_jobs);
     }
     A.n_all.alloc(W * T);
     A.n_kept.alloc(W * T);
@@ -185,6 +209,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     A.seeds.alloc(W);
     A.gen_overflow.alloc(1);
     A.file_order.alloc(T);
+    A.sel_order.alloc(T);
     A.mt_pause.alloc(W * T * mg::kMtN);
     A.actions.alloc(W * action_cap);
     A.actions_c.alloc(W * action_cap);
@@ -207,6 +232,10 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     CK(cudaMemcpyAsync(A.off.p, P.off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(A.cap.p, P.cap.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(A.file_order.p, P.file_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
+    std::vector<int32_t> sel_order(T);
+    for (int t = 0; t < T; ++t) sel_order[t] = t;
+    std::stable_sort(sel_order.begin(), sel_order.end(), [&](int32_t a, int32_t b) { return P.cap[a] > P.cap[b]; });
+    CK(cudaMemcpyAsync(A.sel_order.p, sel_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
 
     mg::WaveBuffers B{};
     B.arr_t = A.arr_t.p;
@@ -222,6 +251,10 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     B.c_compute = A.c_compute.p;
     B.c_transfer = A.c_transfer.p;
     B.c_noise = A.c_noise.p;
+    B.c_order = A.c_order.p;
+    B.tr_cnt = A.tr_cnt.p;
+    B.tr_fab = A.tr_fab.p;
+    B.tr_win = A.tr_win.p;
     B.n_all = A.n_all.p;
     B.n_kept = A.n_kept.p;
     B.mt_pause = A.mt_pause.p;
@@ -237,6 +270,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     B.off = A.off.p;
     B.cap = A.cap.p;
     B.file_order = A.file_order.p;
+    B.sel_order = A.sel_order.p;
     B.gen_overflow = A.gen_overflow.p;
     B.cap_sum = P.cap_sum;
     B.action_cap = action_cap;
@@ -371,6 +405,30 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
                     }
                 }
                 res.comp_off[job + 1] = static_cast<int64_t>(res.comps.size() / 7);
+                if (traces) {
+                    mgb::TraceRows& tr = res.traces[job];
+                    tr.off = P.off;
+                    tr.n_done.resize(T);
+                    for (int i = 0; i < T; ++i) tr.n_done[i] = res.tout[job * T + i].completed_total;
+                    tr.done.assign(tmp.begin(), tmp.begin() + P.cap_sum);
+                    tr.total.assign(tmp.begin() + P.cap_sum, tmp.begin() + 2 * P.cap_sum);
+                    tr.compute.assign(tmp.begin() + 2 * P.cap_sum, tmp.begin() + 3 * P.cap_sum);
+                    tr.transfer.assign(tmp.begin() + 3 * P.cap_sum, tmp.begin() + 4 * P.cap_sum);
+                    tr.noise.assign(tmp.begin() + 4 * P.cap_sum, tmp.begin() + 5 * P.cap_sum);
+                    tr.arrived.resize(P.cap_sum);
+                    tr.bytes.resize(P.cap_sum);
+                    tr.order.resize(P.cap_sum);
+                    CK(cudaMemcpy(tr.arrived.data(), A.arr_t.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(tr.bytes.data(), A.arr_bytes.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(tr.order.data(), A.c_order.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                    tr.n_ticks = n_ticks;
+                    tr.counters.resize(static_cast<size_t>(n_ticks) * T);
+                    tr.fabric.resize(static_cast<size_t>(n_ticks) * R);
+                    CK(cudaMemcpy(tr.counters.data(), A.tr_cnt.p + static_cast<size_t>(k) * n_ticks * T,
+                                  sizeof(mg::CounterRow) * n_ticks * T, cudaMemcpyDeviceToHost));
+                    CK(cudaMemcpy(tr.fabric.data(), A.tr_fab.p + static_cast<size_t>(k) * n_ticks * R,
+                                  sizeof(mg::FabricRow) * n_ticks * R, cudaMemcpyDeviceToHost));
+                }
             }
         }
     }
@@ -429,6 +487,16 @@ void ci(const std::vector<double>& v, double& mean, double& half) {
     double ss = 0.0;
     for (double x : v) ss += (x - mean) * (x - mean);
     half = 1.96 * std::sqrt(ss / n) / std::sqrt(n);
+}
+
+// RunResult of run 0 + its files (engine.cpp:889-892)
+std::string write_artifacts(const migsim_batch_result& res, const std::string& dir, bool traces);
+
+char* dup_c(const std::string& j) {
+    char* o = static_cast<char*>(std::malloc(j.size() + 1));
+    if (!o) throw std::bad_alloc();
+    std::memcpy(o, j.c_str(), j.size() + 1);
+    return o;
 }
 
 std::string num(double v) {
@@ -512,6 +580,39 @@ int migsim_gpu_run_batch(migsim_gpu* g, int32_t scenario_id, const migsim_varian
         *out = res.release();
     });
 }
+
+int migsim_gpu_run_scenario(migsim_gpu* g, int32_t scenario_id, const migsim_variant* variant, uint64_t seed,
+                            const char* out_dir, int32_t write_traces, char** result_json, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
+            throw mgb::ConfigError("unknown scenario id");
+        const std::string dir = out_dir ? out_dir : "";
+        std::vector<mgb::Variant> vs(1);
+        if (variant) vs[0] = to_variant(*variant);
+        migsim_run_opts o{};
+        o.write_traces = (write_traces && !dir.empty()) ? 1 : 0;
+        auto res = std::make_unique<migsim_batch_result>();
+        std::vector<uint64_t> seeds(1, seed);
+        run_batch_checked(g, g->scenarios[static_cast<size_t>(scenario_id)], vs, seeds, o, *res);
+        std::string js = write_artifacts(*res, dir, o.write_traces != 0);
+        if (result_json) *result_json = dup_c(js);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+std::string write_artifacts(const migsim_batch_result& res, const std::string& dir, bool traces) {
+    const mgb::RunResult rr = mgb::assemble(res.spec, res.P, res.variants[0].name, res.seeds[0], res.tout.data(),
+                                            res.quant.data(), res.actions.data(), static_cast<int>(res.act_off[1]),
+                                            res.pauses.data(), static_cast<int>(res.pause_off[1]), res.backlog.data(),
+                                            res.rout[0].n_events);
+    mgb::write_run_artifacts(dir, res.spec, res.P, rr, traces ? &res.traces[0] : nullptr);
+    return mgb::result_to_json(rr);
+}
+}  // namespace
+
+extern "C" {
 
 size_t migsim_batch_n_runs(const migsim_batch_result* r) { return r ? r->n_runs : 0; }
 int migsim_batch_n_tenants(const migsim_batch_result* r) { return r ? r->T : 0; }

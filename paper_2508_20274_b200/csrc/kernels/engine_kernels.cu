@@ -239,8 +239,19 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
         io.c_compute = B.c_compute + base;
         io.c_transfer = B.c_transfer + base;
         io.c_noise = B.c_noise + base;
+        io.c_order = B.c_order + base;
     } else {
         io.c_done = io.c_total = io.c_compute = io.c_transfer = io.c_noise = nullptr;
+        io.c_order = nullptr;
+    }
+    if (B.tr_cnt) {
+        io.tr_cnt = B.tr_cnt + static_cast<int64_t>(r) * S->n_ticks * T;
+        io.tr_fab = B.tr_fab + static_cast<int64_t>(r) * S->n_ticks * S->n_roots;
+        io.tr_win = B.tr_win + static_cast<int64_t>(r) * T;
+    } else {
+        io.tr_cnt = nullptr;
+        io.tr_fab = nullptr;
+        io.tr_win = nullptr;
     }
     Sim<Lanes> sim(*S, Cv, io, st, make_lanes<Lanes>(smem, L, T), td, ctl, rd);
     sim.tn = reinterpret_cast<const PTenant*>(smem + L.sc_tn);

@@ -22,6 +22,10 @@ struct WaveBuffers {
     // [W][cap_sum] arrays
     double *arr_t, *arr_bytes, *arr_mult, *arr_noise, *irq_e, *t_all, *req_ms, *win_lat;
     double *c_done, *c_total, *c_compute, *c_transfer, *c_noise;  // optional
+    int64_t* c_order;                                              // optional, [W][cap_sum]
+    CounterRow* tr_cnt;                                            // optional traces [W][n_ticks][T]
+    FabricRow* tr_fab;                                             //                 [W][n_ticks][R]
+    TailWin* tr_win;                                               //                 [W][T]
     int32_t *n_all, *n_kept;                                       // [W][T]
     uint64_t* mt_pause;                                            // [W][T][312]
     ActionRec* actions;                                            // [W][action_cap]
@@ -36,6 +40,7 @@ struct WaveBuffers {
     const int64_t* off;                                            // [T]
     const int64_t* cap;                                            // [T]
     const int32_t* file_order;                                     // [T]
+    const int32_t* sel_order;                                      // [T] tenants by decreasing cap (select LPT order)
     int32_t* gen_overflow;                                         // [1]
     int64_t cap_sum;
     int32_t action_cap, pause_cap;

@@ -22,6 +22,7 @@ HOSTSIM_SO = os.path.join(ROOT, "tests", "native", "_build", "libhostsim.so")
 PRODUCT_SO = os.path.join(ROOT, "paper_2508_20274_b200", "_lib", "libmigsim_b200.so")
 SCEN_DIR = os.path.join(ROOT, "tests", "golden", "scenarios")
 CONFIG_DIR = os.path.join(ROOT, "scenarios")
+NLOHMANN = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
 
 GOLDEN_SCENARIOS = [os.path.join(SCEN_DIR, f"{n}.yaml") for n in ("default", "llm", "stability", "unstable")]
 CONFIG_SCENARIOS = [os.path.join(CONFIG_DIR, f) for f in ("c1_single_host.yaml", "c2_cluster16.yaml",
@@ -31,14 +32,16 @@ CONFIG_SCENARIOS = [os.path.join(CONFIG_DIR, f) for f in ("c1_single_host.yaml",
 def build_hostsim() -> str:
     src = os.path.join(ROOT, "tests", "native", "hostsim.cpp")
     host = os.path.join(ROOT, "paper_2508_20274_b200", "csrc", "host")
-    deps = [src] + [os.path.join(host, f) for f in ("scenario.cpp", "packer.cpp", "result_json.cpp")]
+    deps = [src] + [os.path.join(host, f) for f in ("scenario.cpp", "packer.cpp", "result_json.cpp", "artifacts.cpp")]
     hdr_dir = os.path.join(ROOT, "paper_2508_20274_b200", "csrc", "common")
-    newest = max(os.path.getmtime(p) for p in deps + [os.path.join(hdr_dir, f) for f in os.listdir(hdr_dir)])
+    hdrs = [os.path.join(hdr_dir, f) for f in os.listdir(hdr_dir)] + [
+        os.path.join(host, f) for f in os.listdir(host) if f.endswith(".hpp")]
+    newest = max(os.path.getmtime(p) for p in deps + hdrs)
     if os.path.exists(HOSTSIM_SO) and os.path.getmtime(HOSTSIM_SO) >= newest:
         return HOSTSIM_SO
     os.makedirs(os.path.dirname(HOSTSIM_SO), exist_ok=True)
     vmap = os.path.join(ROOT, "tests", "native", "exports.map")
-    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-static-libstdc++",
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-static-libstdc++", f"-I{NLOHMANN}",
            "-static-libgcc", f"-Wl,--version-script={vmap}", "-o", HOSTSIM_SO] + deps
     subprocess.run(cmd, check=True)
     return HOSTSIM_SO
@@ -81,6 +84,7 @@ def oracle() -> ctypes.CDLL:
         lib.ref_result_completions.argtypes = [vp] + [vp] * 9
         lib.ref_result_audit.argtypes = [vp, cp, cp, ctypes.POINTER(vp)]
         lib.ref_result_free.argtypes = [vp]
+        lib.ref_run_artifacts.argtypes = [cp, cp, ctypes.c_uint64, cp, ctypes.c_int]
         lib.ref_run_batch.restype = ctypes.c_double
         lib.ref_run_batch.argtypes = [cp, ctypes.POINTER(cp), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                       ctypes.c_int, cp, vp, vp, vp, vp]
@@ -106,6 +110,8 @@ def hostsim() -> ctypes.CDLL:
         lib.hostsim_run.restype = vp
         lib.hostsim_run.argtypes = [ctypes.c_char_p, ctypes.c_uint64] + [ctypes.c_int] * 5 + [vp, vp]
         lib.hostsim_free.argtypes = [vp]
+        lib.hostsim_run_artifacts.restype = vp
+        lib.hostsim_run_artifacts.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_char_p]
         lib.hostsim_arrivals.restype = ctypes.c_long
         lib.hostsim_arrivals.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int, vp, ctypes.c_long]
         lib.hostsim_math.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_long]

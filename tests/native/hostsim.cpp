@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../paper_2508_20274_b200/csrc/common/des_core.h"
+#include "../../paper_2508_20274_b200/csrc/host/artifacts.hpp"
 #include "../../paper_2508_20274_b200/csrc/host/packer.hpp"
 #include "../../paper_2508_20274_b200/csrc/host/result_json.hpp"
 
@@ -84,9 +85,11 @@ void hostsim_free(void* p) { std::free(p); }
 // Run one replica on the CPU through the engine's own kernel logic.  Flags: -1 keeps the
 // scenario's controller setting.  `comp` (optional) receives 6 arrays of per-completion data
 // in canonical tenant order (tenant, seq, done, total, compute, transfer) -- see keep_completions.
-char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, int placement, int guard,
-                  int keep_completions, double** comp_out, long* n_comp) {
+static char* run_impl(const char* yaml_path, uint64_t seed, int enabled, int mig, int placement, int guard,
+                      int keep_completions, double** comp_out, long* n_comp, const char* out_dir) {
     try {
+        const bool traces = out_dir != nullptr;
+        if (traces) keep_completions = 1;
         const ScenarioSpec spec = load_scenario(yaml_path);
         Variant v;
         v.enabled = enabled;
@@ -99,9 +102,27 @@ char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, in
         Arrivals A = generate(P, seed);
         std::vector<double> req(static_cast<size_t>(P.cap_sum), 0.0), win(static_cast<size_t>(P.cap_sum), 0.0);
         std::vector<double> cd, ct, cc, ctr, cn;
+        std::vector<int64_t> corder;
         if (keep_completions) {
             cd.assign(static_cast<size_t>(P.cap_sum), 0.0);
             ct = cc = ctr = cn = cd;
+            corder.assign(static_cast<size_t>(P.cap_sum), 0);
+        }
+        const int n_ticks = P.scen.n_ticks;
+        std::vector<mg::CounterRow> trc;
+        std::vector<mg::FabricRow> trf;
+        std::vector<mg::TailWin> trw;
+        std::vector<double> trr;
+        if (traces) {
+            trc.resize(static_cast<size_t>(n_ticks) * T);
+            trf.resize(static_cast<size_t>(n_ticks) * R);
+            trw.resize(static_cast<size_t>(T));
+            trr.resize(static_cast<size_t>(T) * 256);
+            for (int i = 0; i < T; ++i) {
+                std::memset(&trw[i], 0, sizeof(mg::TailWin));
+                trw[i].ring = trr.data() + 256 * i;
+                trw[i].cap = 256;
+            }
         }
         std::vector<uint64_t> mt(static_cast<size_t>(T) * mg::kMtN);
         std::vector<mg::ActionRec> acts(65536);
@@ -142,6 +163,12 @@ char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, in
             io.c_compute = cc.data();
             io.c_transfer = ctr.data();
             io.c_noise = cn.data();
+            io.c_order = corder.data();
+        }
+        if (traces) {
+            io.tr_cnt = trc.data();
+            io.tr_fab = trf.data();
+            io.tr_win = trw.data();
         }
         mg::Sim<mg::HostLanes> sim(P.scen, C, io, st, mg::HostLanes{slots}, st.td, st.ctl, st.rd);
         sim.init(P.file_order.data(), reinterpret_cast<double*>(base + L.win), reinterpret_cast<double*>(base + L.vwin));
@@ -161,6 +188,23 @@ char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, in
         }
         RunResult r = assemble(spec, P, "as-is", seed, tout.data(), quant.data(), acts.data(), rout.n_actions,
                                pauses.data(), rout.n_pauses, backlog.data(), rout.n_events);
+        if (traces) {
+            TraceRows tr;
+            tr.off = P.off;
+            for (int i = 0; i < T; ++i) tr.n_done.push_back(tout[i].completed_total);
+            tr.done = cd;
+            tr.total = ct;
+            tr.compute = cc;
+            tr.transfer = ctr;
+            tr.noise = cn;
+            tr.arrived = A.t;
+            tr.bytes = A.bytes;
+            tr.order = corder;
+            tr.n_ticks = n_ticks;
+            tr.counters = trc;
+            tr.fabric = trf;
+            write_run_artifacts(out_dir, spec, P, r, &tr);
+        }
         if (keep_completions && comp_out) {
             long n = 0;
             for (int i = 0; i < T; ++i) n += static_cast<long>(tout[i].completed_total);
@@ -187,6 +231,16 @@ char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, in
         g_err = e.what();
         return nullptr;
     }
+}
+
+char* hostsim_run(const char* yaml_path, uint64_t seed, int enabled, int mig, int placement, int guard,
+                  int keep_completions, double** comp_out, long* n_comp) {
+    return run_impl(yaml_path, seed, enabled, mig, placement, guard, keep_completions, comp_out, n_comp, nullptr);
+}
+
+// run_scenario with files (RunOptions{seed, out_dir, write_traces=true}) through the engine logic
+char* hostsim_run_artifacts(const char* yaml_path, uint64_t seed, const char* out_dir) {
+    return run_impl(yaml_path, seed, -1, -1, -1, -1, 1, nullptr, nullptr, out_dir);
 }
 
 // Arrival records of one tenant (canonical index) as generated by the engine's generator code.

@@ -117,10 +117,14 @@ MIGSIM_API void migsim_batch_result_free(migsim_batch_result* r);
 MIGSIM_API int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off, size_t n_segments, const double* qs,
                       size_t n_q, double* out, double* device_ms, char* err, size_t errlen);
 
-/* Batched experiment plans (harness::run_plan, harness.cpp:114-216): plan in {e1,e2,e3,llm};
- * returns experiment.json (same keys/aggregation: population-sigma CIs in seed order). */
+/* Batched experiment plans (harness::run_plan, harness.cpp:114-216; PlanOptions harness.hpp:84-92):
+ * plan in {e1,e2,e3,llm}; returns experiment.json (same keys/aggregation: population-sigma CIs in
+ * seed order).  With out_dir: experiment.json + summary.csv and <variant>/seed<N>/{actions.jsonl,
+ * summary.json} per job, like the reference (harness.cpp:131-133,208-214). */
 MIGSIM_API int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, int32_t seeds, uint64_t seed_base,
-                    const char* focus_tenant, char** experiment_json, char* err, size_t errlen);
+                    const char* focus_tenant, const char* out_dir, char** experiment_json, char* err, size_t errlen);
+/* harness::render_report (harness.cpp:285-313) of an experiment.json text; host only */
+MIGSIM_API int migsim_render_report(const char* experiment_json, char** report, char* err, size_t errlen);
 MIGSIM_API void migsim_free(void* p);
 
 /* ---- diagnostics used by the parity tests ---------------------------------------------- */

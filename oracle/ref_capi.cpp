@@ -259,6 +259,38 @@ int ref_run_artifacts(const char* scenario_json, const char* overrides_json, uin
     }
 }
 
+// harness::run_plan (harness.cpp:114-216) with out_dir: experiment.json, summary.csv and the per-run
+// <variant>/seed<N>/{actions.jsonl,summary.json}.  `scenario_json_path` is a scenario-v1 document
+// already converted to JSON (the restated loader's input).  Returns the experiment JSON (dump(2)).
+char* ref_run_plan(const char* plan, const char* scenario_json_path, int seeds, uint64_t seed_base, const char* focus,
+                   const char* out_dir, int jobs) {
+    try {
+        harness::PlanOptions o;
+        o.plan = plan;
+        o.scenario_path = scenario_json_path;
+        o.seeds = seeds;
+        o.seed_base = seed_base;
+        o.focus_tenant = focus ? focus : "";
+        o.out_dir = out_dir ? out_dir : "";
+        o.jobs = jobs;
+        auto r = harness::run_plan(o);
+        return dup_str(harness::experiment_json(r).dump(2));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// harness::render_report (harness.cpp:272-313) of an experiment.json text
+char* ref_render_report(const char* experiment_json_text) {
+    try {
+        return dup_str(harness::render_report(nlohmann::json::parse(experiment_json_text)));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 const char* ref_result_json(void* hp) { return static_cast<Handle*>(hp)->json_text.c_str(); }
 
 size_t ref_result_n_completions(void* hp) { return static_cast<Handle*>(hp)->result.completions.size(); }

@@ -13,6 +13,7 @@ from .api import (  # noqa: F401
     ablation_variants,
     load_library,
     main_variants,
+    render_report,
     run_plan,
     run_scenario,
 )
@@ -26,6 +27,7 @@ __all__ = [
     "ablation_variants",
     "load_library",
     "main_variants",
+    "render_report",
     "run_plan",
     "run_scenario",
 ]

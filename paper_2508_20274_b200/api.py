@@ -149,7 +149,8 @@ def load_library() -> ctypes.CDLL:
     ]
     lib.migsim_gpu_run_scenario.argtypes = [vp, ctypes.c_int32, ctypes.POINTER(_Variant), ctypes.c_uint64, cp,
                                             ctypes.c_int32, ctypes.POINTER(vp), cp, sz]
-    lib.migsim_run_plan.argtypes = [vp, cp, cp, ctypes.c_int32, ctypes.c_uint64, cp, ctypes.POINTER(vp), cp, sz]
+    lib.migsim_run_plan.argtypes = [vp, cp, cp, ctypes.c_int32, ctypes.c_uint64, cp, cp, ctypes.POINTER(vp), cp, sz]
+    lib.migsim_render_report.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
     lib.migsim_free.argtypes = [vp]
     _lib_handle = lib
     return lib
@@ -347,11 +348,14 @@ class Engine:
         return out, ms.value
 
     def run_plan(self, plan: str, scenario_path: str, seeds: int = 7, seed_base: int = 1,
-                 focus_tenant: str = "") -> dict:
+                 focus_tenant: str = "", out_dir: str = "") -> dict:
+        """harness::run_plan(PlanOptions{plan, scenario_path, seeds, seed_base, out_dir, focus_tenant})
+        (harness.hpp:84-94) with the replica fan-out as one GPU batch."""
         out = ctypes.c_void_p()
         err = ctypes.create_string_buffer(2048)
         _check(self._lib.migsim_run_plan(self._h, plan.encode(), scenario_path.encode(), seeds, seed_base,
-                                         focus_tenant.encode(), ctypes.byref(out), err, 2048), err)
+                                         focus_tenant.encode(), out_dir.encode() if out_dir else None,
+                                         ctypes.byref(out), err, 2048), err)
         try:
             return json.loads(ctypes.string_at(out.value).decode())
         finally:
@@ -384,6 +388,20 @@ def run_scenario(scenario_path: str, seed: int = 1, variant: Optional[Variant] =
     return out
 
 
-def run_plan(plan: str, scenario_path: str, seeds: int = 7, seed_base: int = 1, focus_tenant: str = "") -> dict:
+def run_plan(plan: str, scenario_path: str, seeds: int = 7, seed_base: int = 1, focus_tenant: str = "",
+             out_dir: str = "") -> dict:
     """harness::run_plan (harness.cpp:114-216) with the replica fan-out as one GPU batch."""
-    return default_engine().run_plan(plan, scenario_path, seeds, seed_base, focus_tenant)
+    return default_engine().run_plan(plan, scenario_path, seeds, seed_base, focus_tenant, out_dir)
+
+
+def render_report(experiment: "dict | str") -> str:
+    """harness::render_report (harness.cpp:285-313): the comparison table of an experiment.json."""
+    lib = load_library()
+    text = experiment if isinstance(experiment, str) else json.dumps(experiment)
+    out = ctypes.c_void_p()
+    err = ctypes.create_string_buffer(1024)
+    _check(lib.migsim_render_report(text.encode(), ctypes.byref(out), err, 1024), err)
+    try:
+        return ctypes.string_at(out.value).decode()
+    finally:
+        lib.migsim_free(out)

@@ -22,6 +22,13 @@ void put_file(const std::string& path, const std::string& text) {
     out << text;
 }
 
+ojson interval_obj(double mean, double half) {
+    ojson j;
+    j["mean"] = mean;
+    j["half_width"] = half;
+    return j;
+}
+
 // control::ActionRecord -> one actions.jsonl object, fixed key order (trace.cpp:98-116)
 ojson action_obj(const ActionRecord& r) {
     ojson j;
@@ -222,6 +229,84 @@ std::string fabric_csv_text(const ScenarioSpec&, const Packed& p, const TraceRow
         }
     }
     return o;
+}
+
+void put_text_file(const std::string& path, const std::string& text) { put_file(path, text); }
+
+std::string experiment_json_text(const std::string& plan, const std::string& scenario, const std::string& focus,
+                                 double wall_s, const std::vector<PlanVariantOut>& vs) {
+    ojson j;
+    j["plan"] = plan;
+    j["scenario"] = scenario;
+    j["focus_tenant"] = focus;
+    j["wall_s"] = wall_s;
+    const PlanVariantOut* base = nullptr;
+    for (const auto& v : vs)
+        if (v.name == "static") {
+            base = &v;
+            break;
+        }
+    ojson variants = ojson::array();
+    for (const auto& v : vs) {
+        ojson e;
+        e["name"] = v.name;
+        e["seeds"] = v.seeds;
+        e["p99_ms"] = v.p99_ms;
+        e["miss_rate"] = v.miss_rate;
+        e["throughput_hz"] = v.throughput_hz;
+        e["p99_ci"] = interval_obj(v.mean[0], v.half[0]);
+        e["miss_ci"] = interval_obj(v.mean[1], v.half[1]);
+        e["throughput_ci"] = interval_obj(v.mean[2], v.half[2]);
+        if (base && v.name != "static" && base->mean[0] > 0.0) {
+            e["p99_delta_pct"] = 100.0 * (v.mean[0] - base->mean[0]) / base->mean[0];
+            if (base->mean[1] > 0.0) e["miss_delta_pct"] = 100.0 * (v.mean[1] - base->mean[1]) / base->mean[1];
+            if (base->mean[2] > 0.0)
+                e["throughput_delta_pct"] = 100.0 * (v.mean[2] - base->mean[2]) / base->mean[2];
+        }
+        variants.push_back(std::move(e));
+    }
+    j["variants"] = std::move(variants);
+    return j.dump(2);
+}
+
+std::string experiment_csv_text(const std::vector<PlanVariantOut>& vs) {
+    std::string out = "variant,seed,p99_ms,miss_rate,throughput_hz\n";
+    char buf[160];
+    for (const auto& v : vs)
+        for (size_t i = 0; i < v.seeds.size(); ++i) {
+            std::snprintf(buf, sizeof(buf), "%s,%llu,%.9g,%.9g,%.9g\n", v.name.c_str(),
+                          static_cast<unsigned long long>(v.seeds[i]), v.p99_ms[i], v.miss_rate[i], v.throughput_hz[i]);
+            out += buf;
+        }
+    return out;
+}
+
+std::string render_report_text(const std::string& text) {
+    const nlohmann::json e = nlohmann::json::parse(text);
+    std::string out = "plan: " + e.value("plan", std::string("?")) + "  scenario: " +
+                      e.value("scenario", std::string("?")) + "  tenant: " + e.value("focus_tenant", std::string("?")) +
+                      "\n\n";
+    char line[240];
+    std::snprintf(line, sizeof(line), "%-16s %7s %22s %14s %16s %12s\n", "variant", "seeds", "p99_ms (CI)", "vs static",
+                  "miss_rate", "thr_hz");
+    out += line;
+    out += std::string(92, '-') + "\n";
+    if (!e.contains("variants")) return out;
+    for (const auto& v : e["variants"]) {
+        const auto& p99 = v["p99_ci"];
+        char ci[48];
+        std::snprintf(ci, sizeof(ci), "%.2f +/- %.2f", p99["mean"].get<double>(), p99["half_width"].get<double>());
+        char delta[24];
+        if (v.contains("p99_delta_pct"))
+            std::snprintf(delta, sizeof(delta), "%+.1f%%", v["p99_delta_pct"].get<double>());
+        else
+            std::snprintf(delta, sizeof(delta), "-");
+        std::snprintf(line, sizeof(line), "%-16s %7zu %22s %14s %16.4f %12.2f\n", v["name"].get<std::string>().c_str(),
+                      v["seeds"].size(), ci, delta, v["miss_ci"]["mean"].get<double>(),
+                      v["throughput_ci"]["mean"].get<double>());
+        out += line;
+    }
+    return out;
 }
 
 void write_run_artifacts(const std::string& out_dir, const ScenarioSpec& spec, const Packed& p, const RunResult& r,

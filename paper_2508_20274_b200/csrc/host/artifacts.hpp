@@ -34,6 +34,21 @@ std::string requests_csv_text(const Packed& p, const TraceRows& t);
 std::string counters_csv_text(const Packed& p, const TraceRows& t);
 std::string fabric_csv_text(const ScenarioSpec& spec, const Packed& p, const TraceRows& t);
 
+// harness::ExperimentResult aggregates (harness.hpp:54-73) of one plan
+struct PlanVariantOut {
+    std::string name;
+    std::vector<uint64_t> seeds;
+    std::vector<double> p99_ms, miss_rate, throughput_hz;  // per seed
+    double mean[3] = {0, 0, 0}, half[3] = {0, 0, 0};        // p99, miss, throughput CIs
+};
+// experiment.json body (harness.cpp:235-269, dump(2)), summary.csv (harness.cpp:271-283),
+// render_report of an experiment.json text (harness.cpp:285-313)
+std::string experiment_json_text(const std::string& plan, const std::string& scenario, const std::string& focus,
+                                 double wall_s, const std::vector<PlanVariantOut>& v);
+std::string experiment_csv_text(const std::vector<PlanVariantOut>& v);
+std::string render_report_text(const std::string& experiment_json);
+void put_text_file(const std::string& path, const std::string& text);
+
 // engine::run_scenario's file side (engine.cpp:279-288, 889-892): creates out_dir, writes the three
 // trace streams when `traces` is non-null, then actions.jsonl and summary.json.
 void write_run_artifacts(const std::string& out_dir, const ScenarioSpec& spec, const Packed& p, const RunResult& r,

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -704,7 +705,7 @@ int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off,
 }
 
 int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, int32_t n_seeds, uint64_t seed_base,
-                    const char* focus_tenant, char** experiment_json, char* err, size_t errlen) {
+                    const char* focus_tenant, const char* out_dir, char** experiment_json, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         const auto wall0 = std::chrono::steady_clock::now();
         if (n_seeds < 1) throw mgb::ConfigError("experiment needs at least one seed");
@@ -768,58 +769,45 @@ int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, 
         for (int i = 0; i < res.T; ++i)
             if (res.P.tenant_ids[static_cast<size_t>(i)] == focus) fidx = i;
         const double window_s = base.duration_s - base.measure_start_s;
-        struct Agg {
-            std::vector<double> p99, miss, thr;
-            double m[3], h[3];
-        };
-        std::vector<Agg> agg(vs.size());
+        std::vector<mgb::PlanVariantOut> agg(vs.size());
+        for (size_t v = 0; v < vs.size(); ++v) agg[v].name = vs[v].name;
+        const std::string dir = out_dir ? out_dir : "";
         for (size_t run = 0; run < res.n_runs; ++run) {
-            Agg& a = agg[run / seeds.size()];
+            mgb::PlanVariantOut& a = agg[run / seeds.size()];
+            a.seeds.push_back(seeds[run % seeds.size()]);
             const mg::TenantOut& o = res.tout[run * res.T + fidx];
             const double c = static_cast<double>(o.completed_window);
-            a.p99.push_back(o.completed_window ? res.quant[(run * res.T + fidx) * 4 + 2] : 0.0);
-            a.miss.push_back(o.completed_window ? static_cast<double>(o.window_misses) / c : 0.0);
+            a.p99_ms.push_back(o.completed_window ? res.quant[(run * res.T + fidx) * 4 + 2] : 0.0);
+            a.miss_rate.push_back(o.completed_window ? static_cast<double>(o.window_misses) / c : 0.0);
             double thr = 0.0;
             for (int i = 0; i < res.T; ++i) {
                 const mg::TenantOut& x = res.tout[run * res.T + i];
                 thr += x.completed_window ? static_cast<double>(x.completed_window) / window_s : 0.0;
             }
-            a.thr.push_back(thr);
+            a.throughput_hz.push_back(thr);
+            if (!dir.empty()) {  // per-job artifacts, write_traces=false (harness.cpp:131-133,166-171)
+                const mgb::RunResult rr = mgb::assemble(
+                    res.spec, res.P, a.name, a.seeds.back(), res.tout.data() + run * res.T,
+                    res.quant.data() + run * res.T * 4, res.actions.data() + res.act_off[run],
+                    static_cast<int>(res.act_off[run + 1] - res.act_off[run]), res.pauses.data() + res.pause_off[run],
+                    static_cast<int>(res.pause_off[run + 1] - res.pause_off[run]), res.backlog.data() + run * res.R * 2,
+                    res.rout[run].n_events);
+                mgb::write_run_artifacts(dir + "/" + a.name + "/seed" + std::to_string(a.seeds.back()), res.spec,
+                                         res.P, rr, nullptr);
+            }
         }
         for (auto& a : agg) {
-            ci(a.p99, a.m[0], a.h[0]);
-            ci(a.miss, a.m[1], a.h[1]);
-            ci(a.thr, a.m[2], a.h[2]);
+            ci(a.p99_ms, a.mean[0], a.half[0]);
+            ci(a.miss_rate, a.mean[1], a.half[1]);
+            ci(a.throughput_hz, a.mean[2], a.half[2]);
         }
-        const Agg* st = nullptr;
-        for (size_t v = 0; v < vs.size(); ++v)
-            if (vs[v].name == "static") st = &agg[v];
         const double wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-        std::string j = "{\"plan\":" + std::string("\"") + mgb::json_escape(p) + "\",\"scenario\":\"" +
-                        mgb::json_escape(base.name) + "\",\"focus_tenant\":\"" + mgb::json_escape(focus) +
-                        "\",\"wall_s\":" + num(wall_s) + ",\"variants\":[";
-        for (size_t v = 0; v < vs.size(); ++v) {
-            const Agg& a = agg[v];
-            if (v) j += ",";
-            j += "{\"name\":\"" + mgb::json_escape(vs[v].name) + "\",\"seeds\":[";
-            for (size_t s = 0; s < seeds.size(); ++s) j += (s ? "," : "") + std::to_string(seeds[s]);
-            auto arr = [&](const std::vector<double>& x) {
-                std::string o = "[";
-                for (size_t i = 0; i < x.size(); ++i) o += (i ? "," : "") + num(x[i]);
-                return o + "]";
-            };
-            j += "],\"p99_ms\":" + arr(a.p99) + ",\"miss_rate\":" + arr(a.miss) + ",\"throughput_hz\":" + arr(a.thr);
-            const char* names[3] = {"p99_ci", "miss_ci", "throughput_ci"};
-            for (int k = 0; k < 3; ++k)
-                j += ",\"" + std::string(names[k]) + "\":{\"mean\":" + num(a.m[k]) + ",\"half_width\":" + num(a.h[k]) + "}";
-            if (st && vs[v].name != "static" && st->m[0] > 0.0) {
-                j += ",\"p99_delta_pct\":" + num(100.0 * (a.m[0] - st->m[0]) / st->m[0]);
-                if (st->m[1] > 0.0) j += ",\"miss_delta_pct\":" + num(100.0 * (a.m[1] - st->m[1]) / st->m[1]);
-                if (st->m[2] > 0.0) j += ",\"throughput_delta_pct\":" + num(100.0 * (a.m[2] - st->m[2]) / st->m[2]);
-            }
-            j += "}";
+        const std::string j = mgb::experiment_json_text(p, base.name, focus, wall_s, agg);
+        if (!dir.empty()) {  // harness.cpp:208-214
+            std::filesystem::create_directories(dir);
+            mgb::put_text_file(dir + "/experiment.json", j + "\n");
+            mgb::put_text_file(dir + "/summary.csv", mgb::experiment_csv_text(agg));
         }
-        j += "]}";
         char* outp = static_cast<char*>(std::malloc(j.size() + 1));
         std::memcpy(outp, j.c_str(), j.size() + 1);
         *experiment_json = outp;
@@ -827,6 +815,10 @@ int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, 
 }
 
 void migsim_free(void* p) { std::free(p); }
+
+int migsim_render_report(const char* experiment_json, char** report, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { *report = dup_c(mgb::render_report_text(experiment_json ? experiment_json : "")); });
+}
 
 int migsim_scenario_dump(const char* path, char** json, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {

@@ -85,6 +85,10 @@ def oracle() -> ctypes.CDLL:
         lib.ref_result_audit.argtypes = [vp, cp, cp, ctypes.POINTER(vp)]
         lib.ref_result_free.argtypes = [vp]
         lib.ref_run_artifacts.argtypes = [cp, cp, ctypes.c_uint64, cp, ctypes.c_int]
+        lib.ref_run_plan.restype = vp
+        lib.ref_run_plan.argtypes = [cp, cp, ctypes.c_int, ctypes.c_uint64, cp, cp, ctypes.c_int]
+        lib.ref_render_report.restype = vp
+        lib.ref_render_report.argtypes = [cp]
         lib.ref_run_batch.restype = ctypes.c_double
         lib.ref_run_batch.argtypes = [cp, ctypes.POINTER(cp), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                       ctypes.c_int, cp, vp, vp, vp, vp]

@@ -80,3 +80,67 @@ def test_gpu_artifacts_without_traces_and_determinism(engine, tmp_path):
     assert sorted(os.listdir(a)) == sorted(os.listdir(ref)) == ["actions.jsonl", "summary.json"]
     assert _same_files(ref, a, ["actions.jsonl", "summary.json"]) == []
     assert _same_files(a, b, ["actions.jsonl", "summary.json"]) == []
+
+
+# ---- harness plans: experiment.json / summary.csv / per-job artifacts, render_report ----------
+
+def _ref_plan(plan, path, seeds, seed_base, out_dir, tmp_path):
+    """harness::run_plan of the reference (PlanOptions with out_dir); returns experiment json."""
+    import ctypes
+    import json
+
+    jpath = tmp_path / "scenario.json"
+    jpath.write_bytes(scenario_json(path))
+    lib = oracle()
+    p = lib.ref_run_plan(plan.encode(), str(jpath).encode(), seeds, seed_base, None,
+                         str(out_dir).encode() if out_dir else None, 0)
+    assert p, lib.ref_last_error()
+    try:
+        return json.loads(ctypes.string_at(p).decode())
+    finally:
+        lib.ref_free(p)
+
+
+def test_render_report_matches_reference(tmp_path):
+    """render_report (harness.cpp:285-313) is host code: our C-ABI formats the reference's own
+    experiment.json exactly like the reference (no GPU needed)."""
+    import ctypes
+    import json
+
+    from paper_2508_20274_b200 import render_report
+
+    exp = _ref_plan("e1", GOLDEN_SCENARIOS[1], 2, 5, None, tmp_path)
+    text = json.dumps(exp)
+    lib = oracle()
+    p = lib.ref_render_report(text.encode())
+    assert p, lib.ref_last_error()
+    ref = ctypes.string_at(p).decode()
+    lib.ref_free(p)
+    assert render_report(text) == ref
+    assert "vs static" in ref
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("plan", ["e1", "e2"])
+def test_gpu_plan_artifacts_match_reference(engine, tmp_path, plan):
+    """run_plan with out_dir: summary.csv and every <variant>/seed<N>/ file byte-identical to the
+    reference harness; experiment.json identical except the wall-clock field."""
+    import json
+
+    path = GOLDEN_SCENARIOS[1]
+    ref_dir, my_dir = tmp_path / "ref", tmp_path / "mine"
+    _ref_plan(plan, path, 3, 21, ref_dir, tmp_path)
+    mine = engine.run_plan(plan, path, seeds=3, seed_base=21, out_dir=str(my_dir))
+    assert _same_files(ref_dir, my_dir, ["summary.csv"]) == []
+    rj = json.loads((ref_dir / "experiment.json").read_text())
+    mj = json.loads((my_dir / "experiment.json").read_text())
+    rj.pop("wall_s"), mj.pop("wall_s"), mine.pop("wall_s")
+    assert rj == mj == mine
+    runs = 0
+    for v in os.listdir(ref_dir):
+        if not (ref_dir / v).is_dir():
+            continue
+        for sd in os.listdir(ref_dir / v):
+            assert _same_files(ref_dir / v / sd, my_dir / v / sd, ["actions.jsonl", "summary.json"]) == []
+            runs += 1
+    assert runs == 3 * len(mine["variants"])

@@ -117,6 +117,25 @@ MIGSIM_API void migsim_batch_result_free(migsim_batch_result* r);
 MIGSIM_API int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off, size_t n_segments, const double* qs,
                       size_t n_q, double* out, double* device_ms, char* err, size_t errlen);
 
+/* Batched admission control: Controller::admit (controller.cpp:637-692; declared controller.hpp:
+ * 152-153) for n independent cases on the GPU -- exhaustive placement-candidate scoring over every
+ * (host, gpu).  Tenants are the loaded scenario's, canonical (lexicographic id) order, T of them;
+ * case c requests tenant tenant[c] at MIG profile profile[c] (lattice index 0..4 = 1g..7g) given
+ * TenantStates admitted/host/gpu_id/first/count [n][T] and the ClusterSnapshot fields the scoring
+ * reads: tenant_pcie_Bps, tenant_host_io_Bps [n][T] and irq_recent [n][n_hosts] (bit g = core
+ * group g of that host had a recent IRQ burst).  A fresh controller is assumed (first retry).
+ * outcome: 0 admitted, 1 queued, 2 rejected; reason: 0 none, 1 service rate, 2 no feasible slot,
+ * 3 queue timeout. */
+typedef struct migsim_admit_decision {
+    int32_t outcome, host, gpu, first, count, profile, reason, pad;
+    double score; /* placement_score(...).total() of the chosen slot */
+} migsim_admit_decision;
+MIGSIM_API int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n_cases, const int32_t* tenant,
+                     const int32_t* profile, const int32_t* admitted, const int32_t* host, const int32_t* gpu_id,
+                     const int32_t* first, const int32_t* count, const double* tenant_pcie_Bps,
+                     const double* tenant_host_io_Bps, const uint32_t* irq_recent, migsim_admit_decision* out,
+                     double* device_ms, char* err, size_t errlen);
+
 /* Batched experiment plans (harness::run_plan, harness.cpp:114-216; PlanOptions harness.hpp:84-92):
  * plan in {e1,e2,e3,llm}; returns experiment.json (same keys/aggregation: population-sigma CIs in
  * seed order).  With out_dir: experiment.json + summary.csv and <variant>/seed<N>/{actions.jsonl,

@@ -8,6 +8,7 @@
 // itself, timed on the box's host cores.
 #include <json.hpp>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstdlib>
@@ -19,6 +20,7 @@
 #include <vector>
 
 #include "migsim/audit.hpp"
+#include "migsim/controller.hpp"
 #include "migsim/engine.hpp"
 #include "migsim/fabric.hpp"
 #include "migsim/harness.hpp"
@@ -288,6 +290,66 @@ char* ref_render_report(const char* experiment_json_text) {
     } catch (const std::exception& e) {
         g_err = e.what();
         return nullptr;
+    }
+}
+
+// Controller::admit (controller.cpp:637-692) on explicit cases: tenants in canonical (lexicographic
+// id) order, states [n][T] (admitted, host, gpu id, first, count), snapshot fields [n][T] and
+// irq_recent [n][H] bitmasks, request (tenant index, lattice index).  A fresh Controller per case.
+// out: [n][6] ints (outcome 0/1/2, host, gpu, first, count, reason code) and score[n].
+int ref_admit(const char* scenario_json, int n, const int32_t* tenant, const int32_t* profile,
+              const int32_t* admitted, const int32_t* host, const int32_t* gpu_id, const int32_t* first,
+              const int32_t* count, const double* pcie, const double* hio, const uint32_t* irq, int32_t* out,
+              double* score) {
+    try {
+        const auto spec = scenario::parse_scenario(scenario_json, "<scenario>");
+        std::vector<const scenario::TenantEntry*> canon;
+        for (const auto& t : spec.tenants) canon.push_back(&t);
+        std::sort(canon.begin(), canon.end(),
+                  [](const scenario::TenantEntry* a, const scenario::TenantEntry* b) { return a->spec.id < b->spec.id; });
+        const int T = static_cast<int>(canon.size());
+        const int H = static_cast<int>(spec.topology.hosts.size());
+        const auto& lattice = model::mig_lattice();
+        for (int c = 0; c < n; ++c) {
+            control::TenantStates states;
+            control::ClusterSnapshot snap;
+            for (int j = 0; j < T; ++j) {
+                const int x = c * T + j;
+                model::TenantState st;
+                st.spec = &canon[j]->spec;
+                st.placement = {host[x], gpu_id[x], {first[x], count[x]}};
+                st.profile = lattice[0];
+                for (const auto& p : lattice)
+                    if (p.slices == count[x]) st.profile = p;
+                st.status = admitted[x] ? model::TenantStatus::admitted : model::TenantStatus::queued;
+                states[canon[j]->spec.id] = st;
+                snap.tenant_pcie_Bps[canon[j]->spec.id] = pcie[x];
+                snap.tenant_host_io_Bps[canon[j]->spec.id] = hio[x];
+            }
+            for (int h = 0; h < H; ++h)
+                for (int g = 0; g < 32; ++g)
+                    if ((irq[c * H + h] >> g) & 1u) snap.irq_recent.insert({h, g});
+            control::Controller ctl(spec.controller, spec.topology);
+            const auto d = ctl.admit(canon[tenant[c]]->spec, lattice[profile[c]].name, snap, states);
+            int32_t* o = out + 6 * c;
+            o[0] = d.outcome == control::AdmissionOutcome::admitted ? 0
+                   : d.outcome == control::AdmissionOutcome::queued ? 1 : 2;
+            o[1] = o[0] == 0 ? d.placement.host : -1;
+            o[2] = o[0] == 0 ? d.placement.gpu : -1;
+            o[3] = o[0] == 0 ? d.placement.slices.first : -1;
+            o[4] = o[0] == 0 ? d.placement.slices.count : -1;
+            o[5] = o[0] == 0 ? 0
+                   : d.reason.find("service rate") != std::string::npos ? 1
+                   : d.reason.find("timeout") != std::string::npos ? 3 : 2;
+            score[c] = 0.0;
+            if (o[0] == 0)
+                score[c] = control::placement_score(spec.topology, states, snap, canon[tenant[c]]->spec.id,
+                                                    d.placement.host, d.placement.gpu).total();
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
     }
 }
 

@@ -151,6 +151,7 @@ def load_library() -> ctypes.CDLL:
                                             ctypes.c_int32, ctypes.POINTER(vp), cp, sz]
     lib.migsim_run_plan.argtypes = [vp, cp, cp, ctypes.c_int32, ctypes.c_uint64, cp, cp, ctypes.POINTER(vp), cp, sz]
     lib.migsim_render_report.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
+    lib.migsim_gpu_admit.argtypes = [vp, ctypes.c_int32, sz] + [vp] * 11 + [ctypes.POINTER(ctypes.c_double), cp, sz]
     lib.migsim_free.argtypes = [vp]
     _lib_handle = lib
     return lib
@@ -254,6 +255,11 @@ class BatchResult:
             pass
 
 
+ADMIT_DTYPE = np.dtype([("outcome", np.int32), ("host", np.int32), ("gpu", np.int32), ("first", np.int32),
+                        ("count", np.int32), ("profile", np.int32), ("reason", np.int32), ("pad", np.int32),
+                        ("score", np.float64)])
+
+
 class Engine:
     """One B200 device (C-ABI handle)."""
 
@@ -332,6 +338,27 @@ class Engine:
             return json.loads(ctypes.string_at(out.value).decode())
         finally:
             self._lib.migsim_free(out)
+
+    def admit(self, sid: int, tenant, profile, admitted, host, gpu, first, count, tenant_pcie_Bps,
+              tenant_host_io_Bps, irq_recent) -> (np.ndarray, float):
+        """Controller::admit (controller.cpp:637-692) for n independent cases on the GPU.
+
+        tenant/profile: [n] canonical tenant index / MIG lattice index of each request;
+        admitted/host/gpu/first/count and tenant_pcie_Bps/tenant_host_io_Bps: [n, T] TenantStates and
+        snapshot fields (tenants in canonical order); irq_recent: [n, n_hosts] core-group bitmasks.
+        Returns (decisions, device_ms); decisions has fields outcome (0 admitted, 1 queued,
+        2 rejected), host, gpu, first, count, profile, reason, score."""
+        i32 = lambda a: np.ascontiguousarray(np.asarray(a, np.int32))  # noqa: E731
+        f64 = lambda a: np.ascontiguousarray(np.asarray(a, np.float64))  # noqa: E731
+        args = [i32(tenant), i32(profile), i32(admitted), i32(host), i32(gpu), i32(first), i32(count),
+                f64(tenant_pcie_Bps), f64(tenant_host_io_Bps), np.ascontiguousarray(np.asarray(irq_recent, np.uint32))]
+        n = len(args[0])
+        out = np.zeros(n, dtype=ADMIT_DTYPE)
+        ms = ctypes.c_double()
+        err = ctypes.create_string_buffer(1024)
+        _check(self._lib.migsim_gpu_admit(self._h, sid, n, *[a.ctypes.data for a in args], out.ctypes.data,
+                                          ctypes.byref(ms), err, 1024), err)
+        return out, ms.value
 
     def select(self, segments: Sequence[np.ndarray], qs: Sequence[float]) -> (np.ndarray, float):
         """Nearest-rank quantiles of each segment on the GPU; returns (out[n_seg, n_q], device_ms)."""

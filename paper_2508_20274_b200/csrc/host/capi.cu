@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../../include/migsim_b200.h"
+#include "../kernels/admit_kernel.cuh"
 #include "../kernels/engine_kernels.cuh"
 #include "artifacts.hpp"
 #include "packer.hpp"
@@ -815,6 +816,84 @@ int migsim_run_plan(migsim_gpu* g, const char* plan, const char* scenario_path, 
 }
 
 void migsim_free(void* p) { std::free(p); }
+
+int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n, const int32_t* tenant, const int32_t* profile,
+                     const int32_t* admitted, const int32_t* host, const int32_t* gpu_id, const int32_t* first,
+                     const int32_t* count, const double* tenant_pcie_Bps, const double* tenant_host_io_Bps,
+                     const uint32_t* irq_recent, migsim_admit_decision* out, double* device_ms, char* err,
+                     size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
+            throw mgb::ConfigError("unknown scenario id");
+        CK(cudaSetDevice(g->device));
+        const mgb::ScenarioSpec& spec = g->scenarios[static_cast<size_t>(scenario_id)];
+        const mgb::Packed P = mgb::pack(spec, {});
+        const int T = P.scen.n_tenants, H = P.scen.n_hosts;
+        // (host, gpu id) -> canonical GPU index; validate every case on the host
+        std::vector<int32_t> gidx(n * T);
+        auto find_gpu = [&](int h, int id) {
+            for (int k = 0; k < P.scen.n_gpus; ++k)
+                if (P.scen.gpus[k].host == h && P.scen.gpus[k].id == id) return k;
+            return -1;
+        };
+        for (size_t c = 0; c < n; ++c) {
+            if (tenant[c] < 0 || tenant[c] >= T) throw mgb::ConfigError("admit: tenant index out of range");
+            if (profile[c] < 0 || profile[c] >= mg::kNumProfiles) throw mgb::ConfigError("admit: unknown MIG profile");
+            for (int j = 0; j < T; ++j) {
+                const size_t x = c * T + j;
+                gidx[x] = admitted[x] ? find_gpu(host[x], gpu_id[x]) : 0;
+                if (gidx[x] < 0)
+                    throw mgb::ConfigError("admit: no GPU " + std::to_string(gpu_id[x]) + " on host " + std::to_string(host[x]));
+            }
+        }
+        DevBuf<mg::PScenario> dS;
+        DevBuf<int32_t> dt, dp, da, dh, dg, df, dc;
+        DevBuf<double> dpc, dio;
+        DevBuf<uint32_t> dirq;
+        DevBuf<mg::AdmitOut> dout;
+        dS.alloc(1);
+        auto up = [&](auto& buf, const auto* src, size_t cnt) {
+            buf.alloc(cnt ? cnt : 1);
+            if (cnt) CK(cudaMemcpyAsync(buf.p, src, sizeof(*src) * cnt, cudaMemcpyHostToDevice, g->stream));
+        };
+        cudaStream_t s = g->stream;
+        CK(cudaMemcpyAsync(dS.p, &P.scen, sizeof(mg::PScenario), cudaMemcpyHostToDevice, s));
+        up(dt, tenant, n);
+        up(dp, profile, n);
+        up(da, admitted, n * T);
+        up(dh, host, n * T);
+        up(dg, gidx.data(), n * T);
+        up(df, first, n * T);
+        up(dc, count, n * T);
+        up(dpc, tenant_pcie_Bps, n * T);
+        up(dio, tenant_host_io_Bps, n * T);
+        up(dirq, irq_recent, n * H);
+        dout.alloc(n ? n : 1);
+        mg::AdmitCases C{dt.p, dp.p, da.p, dh.p, dg.p, df.p, dc.p, dpc.p, dio.p, dirq.p};
+        CK(cudaEventRecord(g->ev[4], s));
+        if (n) mg::admit_kernel<<<static_cast<unsigned>(n), 32, 0, s>>>(dS.p, C, static_cast<int>(n),
+                                                                       spec.controller.admission_queue_timeout_epochs, dout.p);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(g->ev[5], s));
+        std::vector<mg::AdmitOut> h(n);
+        if (n) CK(cudaMemcpyAsync(h.data(), dout.p, sizeof(mg::AdmitOut) * n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, g->ev[4], g->ev[5]));
+        if (device_ms) *device_ms = ms;
+        for (size_t c = 0; c < n; ++c) {
+            out[c].outcome = h[c].outcome;
+            out[c].host = h[c].host;
+            out[c].gpu = h[c].gpu_id;
+            out[c].first = h[c].first;
+            out[c].count = h[c].count;
+            out[c].profile = h[c].profile;
+            out[c].reason = h[c].reason;
+            out[c].pad = 0;
+            out[c].score = h[c].score;
+        }
+    });
+}
 
 int migsim_render_report(const char* experiment_json, char** report, char* err, size_t errlen) {
     return guarded(err, errlen, [&] { *report = dup_c(mgb::render_report_text(experiment_json ? experiment_json : "")); });

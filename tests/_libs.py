@@ -89,6 +89,7 @@ def oracle() -> ctypes.CDLL:
         lib.ref_run_plan.argtypes = [cp, cp, ctypes.c_int, ctypes.c_uint64, cp, cp, ctypes.c_int]
         lib.ref_render_report.restype = vp
         lib.ref_render_report.argtypes = [cp]
+        lib.ref_admit.argtypes = [cp, ctypes.c_int] + [vp] * 12
         lib.ref_run_batch.restype = ctypes.c_double
         lib.ref_run_batch.argtypes = [cp, ctypes.POINTER(cp), ctypes.c_int, ctypes.c_uint64, ctypes.c_int,
                                       ctypes.c_int, cp, vp, vp, vp, vp]

@@ -327,8 +327,15 @@ MG_HD SimLayout sim_layout(int T, int R, int W, int V, bool rings, int G = 0, in
 // ---------------------------------------------------------------------------------------------
 // The replica simulator.  `Lanes` abstracts the warp: on the device all 32 lanes execute this
 // code redundantly on identical shared-memory state, with the event-slot argmin done lane-parallel.
+// Tenant-set words: 32-bit when the lane-register event slots are used (T <= 10), else 64-bit.
+template <class Lanes>
+struct MaskOf {
+    using type = uint64_t;
+};
+
 template <class Lanes>
 struct Sim {
+    using Mask = typename MaskOf<Lanes>::type;
     const PScenario& S;
     const PController& C;
     ReplicaIO io;
@@ -338,7 +345,7 @@ struct Sim {
     // per-event scalars kept out of shared memory (registers once inlined into the kernel)
     double now;
     uint64_t next_seq, n_events;
-    uint64_t live_resume, live_expire;  // tenants with a live resume / guardrail-expire event
+    Mask live_resume, live_expire;  // tenants with a live resume / guardrail-expire event
     // Working-set arrays held as registers (not re-loaded from SimState) so that, after inlining
     // into the kernel, the compiler sees shared-memory provenance and emits LDS/STS.
     TenantDyn* td;
@@ -379,8 +386,8 @@ struct Sim {
     MG_HD static bool rare_kind(int kind) { return kind == kEvResume || kind == kEvExpire; }
     MG_HD bool any_rare() const { return (live_resume | live_expire) != 0; }
     MG_HD void mark_rare(int kind, int i, bool live) {
-        uint64_t& m = kind == kEvResume ? live_resume : live_expire;
-        m = live ? (m | (1ull << i)) : (m & ~(1ull << i));
+        Mask& m = kind == kEvResume ? live_resume : live_expire;
+        m = live ? (m | (Mask(1) << i)) : (m & ~(Mask(1) << i));
     }
 
     MG_HD void push(int kind, int i, double t) {
@@ -422,7 +429,7 @@ struct Sim {
     }
     MG_HD double root_offered(int r) const {
         double s = 0.0;
-        for (uint64_t m = rd[r].active; m; m &= m - 1) s = fadd(s, td[ctz64(m)].grant);
+        for (Mask m = static_cast<Mask>(rd[r].active); m; m &= m - 1) s = fadd(s, td[ctz64(m)].grant);
         return s;
     }
     MG_HD double host_io(int h) const {
@@ -453,10 +460,17 @@ struct Sim {
         return __builtin_ctzll(m);
 #endif
     }
+    MG_HD static int ctz64(uint32_t m) {
+#if defined(__CUDA_ARCH__)
+        return __ffs(static_cast<int>(m)) - 1;
+#else
+        return __builtin_ctz(m);
+#endif
+    }
 
     // ---- fabric (fabric.cpp:31-87 via engine.cpp:312-347) ----------------------------------
     MG_HD void settle_root(int r) {
-        for (uint64_t m = rd[r].active; m; m &= m - 1) {
+        for (Mask m = static_cast<Mask>(rd[r].active); m; m &= m - 1) {
             TenantDyn& d = td[ctz64(m)];
             const double dt = fsub(now, d.last_settle);
             if (dt > 0.0 && d.grant > 0.0) {
@@ -469,13 +483,13 @@ struct Sim {
     }
 
     MG_HD void reallocate_root(int r) {
-        const uint64_t act = rd[r].active;
+        const Mask act = static_cast<Mask>(rd[r].active);
         const double cap = rt[r].capacity;
         if (act) {
             double wsum = 0.0;
-            for (uint64_t m = act; m; m &= m - 1) wsum = fadd(wsum, spec(ctz64(m)).weight);
+            for (Mask m = act; m; m &= m - 1) wsum = fadd(wsum, spec(ctz64(m)).weight);
             double granted = 0.0;
-            for (uint64_t m = act; m; m &= m - 1) {
+            for (Mask m = act; m; m &= m - 1) {
                 const int i = ctz64(m);
                 const double share = fdiv_exact(fmul(cap, spec(i).weight), wsum);
                 const double c = eff_pcie_cap(i);
@@ -487,14 +501,14 @@ struct Sim {
                 double residual = fsub(cap, granted);
                 for (int iter = 0; iter < 64 && residual > fmul(1e-9, cap); ++iter) {
                     double open_w = 0.0;
-                    for (uint64_t m = act; m; m &= m - 1) {
+                    for (Mask m = act; m; m &= m - 1) {
                         const int i = ctz64(m);
                         const double c = eff_pcie_cap(i);
                         if (!(c > 0.0) || td[i].grant < fsub(c, 1e-12)) open_w = fadd(open_w, spec(i).weight);
                     }
                     if (open_w <= 0.0) break;
                     double moved = 0.0;
-                    for (uint64_t m = act; m; m &= m - 1) {
+                    for (Mask m = act; m; m &= m - 1) {
                         const int i = ctz64(m);
                         const double c = eff_pcie_cap(i);
                         double& g = td[i].grant;
@@ -512,7 +526,7 @@ struct Sim {
                 }
             }
         }
-        for (uint64_t m = act; m; m &= m - 1) {
+        for (Mask m = act; m; m &= m - 1) {
             const int i = ctz64(m);
             TenantDyn& d = td[i];
             d.last_settle = now;

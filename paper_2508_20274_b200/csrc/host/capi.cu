@@ -24,6 +24,10 @@
 
 namespace mg {
 size_t select_smem_bytes();
+size_t select_cluster_smem_bytes();
+int select_cluster_size();
+int select_cluster_threads();
+int select_threads();
 size_t gen_times_smem_bytes();
 }
 
@@ -293,6 +297,12 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     CK(cudaFuncSetAttribute(des, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
     const size_t sel_smem = mg::select_smem_bytes();
     CK(cudaFuncSetAttribute(mg::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sel_smem)));
+    const size_t cl_smem = mg::select_cluster_smem_bytes();
+    CK(cudaFuncSetAttribute(mg::select_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cl_smem)));
+    // MIGSIM_SELECT=cluster: the one-HBM-pass cluster select (same results; measured slower on the
+    // C2 wave, 0.24 vs 0.15 ms -- DESIGN.md section 6)
+    const char* sel_env = std::getenv("MIGSIM_SELECT");
+    const bool sel_cluster = sel_env && std::string(sel_env) == "cluster";
 
     res.tout.resize(n_jobs * T);
     res.quant.resize(n_jobs * T * 4);
@@ -327,7 +337,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         des<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[2], s));
-        mg::select_kernel<<<static_cast<unsigned>(nt), 256, sel_smem, s>>>(B, T, w);
+        if (sel_cluster)
+            mg::select_cluster_kernel<<<static_cast<unsigned>(nt * mg::select_cluster_size()), mg::select_cluster_threads(),
+                                        cl_smem, s>>>(B, T, w);
+        else
+            mg::select_kernel<<<static_cast<unsigned>(nt), mg::select_threads(), sel_smem, s>>>(B, T, w);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[3], s));
         int32_t overflow = 0;
@@ -693,7 +707,7 @@ int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off,
         const size_t sm = mg::select_smem_bytes();
         CK(cudaFuncSetAttribute(mg::select_segments_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
         CK(cudaEventRecord(g->ev[4], s));
-        mg::select_segments_kernel<<<static_cast<unsigned>(n_segments), 256, sm, s>>>(dv.p, doff.p, static_cast<int>(n_segments),
+        mg::select_segments_kernel<<<static_cast<unsigned>(n_segments), mg::select_threads(), sm, s>>>(dv.p, doff.p, static_cast<int>(n_segments),
                                                                                        dq.p, static_cast<int>(n_q), dout.p);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[5], s));

@@ -92,6 +92,11 @@ struct RegLanes {
     __device__ __forceinline__ void clear(int s) { put(s, 0xffffffffu, 0xffffffffu, 0xffffffffu); }
 };
 
+template <>
+struct MaskOf<RegLanes> {
+    using type = uint32_t;  // T <= kRegSlotMaxTenants
+};
+
 template <class Lanes>
 __device__ __forceinline__ Lanes make_lanes(unsigned char* smem, const SimLayout& L, int T);
 template <>

@@ -58,6 +58,8 @@ constexpr int kRegSlotMaxTenants = 10;  // 3T+1 hot slots and 2T rare slots with
 __global__ void des_kernel_reg(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
                                int n_rep, SimLayout L);
 __global__ void select_kernel(WaveBuffers B, int T, int n_rep);
+// same results, one HBM pass: 4-CTA cluster per segment, TMA bulk loads, DSMEM histogram/gather
+__global__ void select_cluster_kernel(WaveBuffers B, int T, int n_rep);
 __global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
                                        const int64_t* __restrict__ dst_off, ActionRec* __restrict__ dst, int n_rep);
 __global__ void compact_pauses_kernel(const PauseRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,

@@ -15,6 +15,8 @@
 //             (one digit compare per bin) and finished by the in-smem radix select.
 //    Groups too large for the gather buffer are refined by another digit pass first.
 // Every result is an element chosen by exact integer ranks: bit-identical to std::sort + index.
+#include <cooperative_groups.h>
+
 #include "engine_kernels.cuh"
 
 namespace mg {
@@ -22,6 +24,7 @@ namespace mg {
 namespace {
 
 constexpr int kSelThreads = 256;
+static_assert(kSelThreads / 32 >= 4 && kSelThreads / 32 <= 32, "one warp per quantile, one scan warp");
 constexpr int kDigit = 12;
 constexpr int kBins = 1 << kDigit;
 constexpr int kMaxQ = 4;
@@ -44,7 +47,7 @@ __device__ __forceinline__ int bitlen64(uint64_t x) { return x ? 64 - __clzll(st
 struct SelSmem {
     uint32_t hist[kBins];
     uint64_t cand[kCand];
-    uint32_t wsum[kSelThreads / 32];
+    uint32_t wsum[32];
     uint64_t qlo[kMaxQ];
     int64_t qrank[kMaxQ];
     int64_t qgroup[kMaxQ];
@@ -61,9 +64,26 @@ struct SelSmem {
     int32_t fits;
 };
 
+// 16-B read-only load with an L2 eviction-priority policy: the first pass over a segment keeps its
+// lines (evict_last) for the gather pass that re-reads them, which then releases them (evict_first).
+__device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t pol) {
+    double2 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint64_t l2_policy(bool keep) {
+    uint64_t pol;
+    if (keep)
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    else
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 // f(key) for every element of v[0..n): 16-B loads, 4 in flight per thread
 template <class F>
-__device__ __forceinline__ void stream_keys(const double* __restrict__ v, int64_t n, F&& f) {
+__device__ __forceinline__ void stream_keys(const double* __restrict__ v, int64_t n, F&& f, bool keep = true) {
+    const uint64_t pol = l2_policy(keep);
     const int tid = threadIdx.x;
     int64_t head = (16 - (reinterpret_cast<uintptr_t>(v) & 15)) / 8 & 1;
     if (head > n) head = n;
@@ -71,26 +91,36 @@ __device__ __forceinline__ void stream_keys(const double* __restrict__ v, int64_
     const double2* v2 = reinterpret_cast<const double2*>(v + head);
     const int64_t n2 = (n - head) / 2;
     int64_t i = tid;
-    for (; i + 3 * kSelThreads < n2; i += 4 * kSelThreads) {
-        const double2 a = __ldg(v2 + i), b = __ldg(v2 + i + kSelThreads), c = __ldg(v2 + i + 2 * kSelThreads),
-                      d = __ldg(v2 + i + 3 * kSelThreads);
-        f(okey(a.x));
-        f(okey(a.y));
-        f(okey(b.x));
-        f(okey(b.y));
-        f(okey(c.x));
-        f(okey(c.y));
-        f(okey(d.x));
-        f(okey(d.y));
+    constexpr int kDepth = 8;  // 16-B loads in flight per thread (128 B): ~128 KB per SM at 4 CTAs
+    const int nthr = blockDim.x;
+    for (; i + (kDepth - 1) * nthr < n2; i += kDepth * nthr) {
+        double2 x[kDepth];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) x[u] = ld_hint(v2 + i + u * nthr, pol);
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+            f(okey(x[u].x));
+            f(okey(x[u].y));
+        }
     }
-    for (; i < n2; i += kSelThreads) {
-        const double2 a = __ldg(v2 + i);
+    for (; i < n2; i += nthr) {
+        const double2 a = ld_hint(v2 + i, pol);
         f(okey(a.x));
         f(okey(a.y));
     }
     const int64_t tail = head + 2 * n2;
     if (tid < n - tail) f(okey(v[tail + tid]));
 }
+
+// A segment in global memory as a key source: every pass but the last keeps its L2 lines.
+struct GlobalSrc {
+    const double* v;
+    int64_t n;
+    template <class F>
+    __device__ __forceinline__ void operator()(F&& f) const { stream_keys(v, n, f, true); }
+    template <class F>
+    __device__ __forceinline__ void last(F&& f) const { stream_keys(v, n, f, false); }
+};
 
 // Block-wide: given per-thread partial count s, return the exclusive prefix of the block.
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t s, uint32_t* wsum) {
@@ -102,50 +132,85 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t s, uint32_t* wsum) 
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    uint32_t base = 0;
-#pragma unroll
-    for (int w = 0; w < kSelThreads / 32; ++w) base += w < warp ? wsum[w] : 0u;
+    if (warp == 0) {  // exclusive scan of the warp totals
+        const int kW = static_cast<int>(blockDim.x) / 32;
+        const uint32_t w = lane < kW ? wsum[lane] : 0u;
+        uint32_t x = w;
+        for (int o = 1; o < kW; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane < kW) wsum[lane] = x - w;
+    }
+    __syncthreads();
+    const uint32_t base = wsum[warp];
     __syncthreads();
     return base + incl - s;
 }
 
 // Exact select of the rank-th smallest among the keys of group [lo, lo + 2^sh) found in
-// keys[0..m) (shared memory): 8-bit radix steps relative to lo; stops as soon as the rank's bin
-// holds a single key.
-__device__ uint64_t smem_select(const uint64_t* keys, int m, int64_t rank, uint64_t lo, int sh, SelSmem& sm) {
-    const int tid = threadIdx.x;
+// keys[0..m) (shared memory) by ONE warp, no block barriers: 8-bit radix steps relative to lo
+// over a warp-private 256-bin histogram; stops as soon as the rank's bin holds a single key.
+// The quantiles of a segment run in parallel, one warp each.
+__device__ uint64_t warp_select(const uint64_t* keys, int m, int64_t rank, uint64_t lo, int sh, uint32_t* hist) {
+    const int lane = threadIdx.x & 31;
     while (sh > 0) {
         const int d = sh < 8 ? sh : 8;
         const int s = sh - d;
-        sm.hist[tid] = 0;  // 256 threads == 256 bins
-        __syncthreads();
-        for (int a = tid; a < m; a += kSelThreads) {
+        for (int b = lane; b < 256; b += 32) hist[b] = 0;
+        __syncwarp();
+        for (int a = lane; a < m; a += 32) {
             const uint64_t k = keys[a];
-            if (in_group(k, lo, sh)) atomicAdd(&sm.hist[static_cast<uint32_t>((k - lo) >> s)], 1u);
+            if (in_group(k, lo, sh)) atomicAdd(&hist[static_cast<uint32_t>((k - lo) >> s)], 1u);
         }
-        __syncthreads();
-        const uint32_t c = sm.hist[tid];
-        const uint32_t below = block_excl_scan(c, sm.wsum);
-        if (rank >= below && rank < static_cast<int64_t>(below) + c) {
-            sm.scr_lo = lo + (static_cast<uint64_t>(tid) << s);
-            sm.scr_rank = rank - below;
-            sm.scr_cnt = static_cast<int32_t>(c);
+        __syncwarp();
+        uint32_t c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            c[j] = hist[lane * 8 + j];
+            tot += c[j];
         }
-        __syncthreads();
-        lo = sm.scr_lo;
-        rank = sm.scr_rank;
-        const int cnt = sm.scr_cnt;
+        uint32_t incl = tot;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int64_t below = static_cast<int64_t>(incl - tot);
+        int bin = -1;
+        int64_t acc = below;
+        uint32_t cnt = 0;
+        if (rank >= below && rank < below + tot) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (bin < 0) {
+                    if (acc + c[j] > rank) {
+                        bin = lane * 8 + j;
+                        cnt = c[j];
+                    } else {
+                        acc += c[j];
+                    }
+                }
+        }
+        const int owner = __ffs(__ballot_sync(0xffffffffu, bin >= 0)) - 1;
+        bin = __shfl_sync(0xffffffffu, bin, owner);
+        acc = __shfl_sync(0xffffffffu, acc, owner);
+        cnt = __shfl_sync(0xffffffffu, cnt, owner);
+        lo += static_cast<uint64_t>(bin) << s;
+        rank -= acc;
         sh = s;
-        __syncthreads();
+        __syncwarp();
         if (cnt == 1 && sh > 0) {  // the only key of the bin is the answer
-            for (int a = tid; a < m; a += kSelThreads) {
+            uint64_t hit = 0;
+            bool found = false;
+            for (int a = lane; a < m && !found; a += 32) {
                 const uint64_t k = keys[a];
-                if (in_group(k, lo, sh)) sm.scr_lo = k;
+                if (in_group(k, lo, sh)) {
+                    hit = k;
+                    found = true;
+                }
             }
-            __syncthreads();
-            lo = sm.scr_lo;
-            __syncthreads();
-            return lo;
+            const int who = __ffs(__ballot_sync(0xffffffffu, found)) - 1;
+            return __shfl_sync(0xffffffffu, hit, who);
         }
     }
     return lo;
@@ -159,7 +224,7 @@ __device__ void digit_pass(Src&& src, uint64_t lo, int sh, bool all_in, int nq, 
     const int tid = threadIdx.x;
     const int d = sh < kDigit ? sh : kDigit;
     const int s = sh - d;
-    for (int b = tid; b < kBins; b += kSelThreads) sm.hist[b] = 0;
+    for (int b = tid; b < kBins; b += static_cast<int>(blockDim.x)) sm.hist[b] = 0;
     __syncthreads();
     if (all_in)
         src([&](uint64_t k) { atomicAdd(&sm.hist[static_cast<uint32_t>((k - lo) >> s)], 1u); });
@@ -168,7 +233,7 @@ __device__ void digit_pass(Src&& src, uint64_t lo, int sh, bool all_in, int nq, 
             if (in_group(k, lo, sh)) atomicAdd(&sm.hist[static_cast<uint32_t>((k - lo) >> s)], 1u);
         });
     __syncthreads();
-    constexpr int per = kBins / kSelThreads;
+    const int per = kBins / static_cast<int>(blockDim.x);
     uint32_t cnt = 0;
     for (int b = 0; b < per; ++b) cnt += sm.hist[tid * per + b];
     const int64_t below = block_excl_scan(cnt, sm.wsum);
@@ -272,7 +337,7 @@ __device__ void select_in(Src&& src, int64_t n, uint64_t kmin, uint64_t kmax, co
             gb[g] = g < ng ? static_cast<uint32_t>((glo[g] - kmin) >> s1) : 0xffffffffu;
             gof[g] = g < ng ? go[g] : 0;
         }
-        src([&](uint64_t k) {
+        src.last([&](uint64_t k) {
             const uint32_t dg = static_cast<uint32_t>((k - kmin) >> s1);
 #pragma unroll
             for (int g = 0; g < kMaxQ; ++g)
@@ -282,7 +347,7 @@ __device__ void select_in(Src&& src, int64_t n, uint64_t kmin, uint64_t kmax, co
                 }
         });
     } else {
-        src([&](uint64_t k) {
+        src.last([&](uint64_t k) {
             for (int g = 0; g < ng; ++g)
                 if (in_group(k, glo[g], gsh[g])) {
                     const uint32_t at = atomicAdd(&sm.qfill[go[g]], 1u);
@@ -291,14 +356,16 @@ __device__ void select_in(Src&& src, int64_t n, uint64_t kmin, uint64_t kmax, co
         });
     }
     __syncthreads();
-    for (int q = 0; q < nq; ++q) {
-        if (sm.qdone[q]) continue;
-        const int o = sm.qslot[q];
-        const uint64_t r = smem_select(sm.cand + sm.qbase[o], static_cast<int>(sm.qgroup[o]), sm.qrank[q], sm.qlo[q],
-                                       sm.qshift[q], sm);
-        if (tid == 0) sm.qresult[q] = kval(r);
-        __syncthreads();
+    {
+        const int q = tid >> 5;  // warp q finishes quantile q
+        if (q < nq && !sm.qdone[q]) {
+            const int o = sm.qslot[q];
+            const uint64_t r = warp_select(sm.cand + sm.qbase[o], static_cast<int>(sm.qgroup[o]), sm.qrank[q], sm.qlo[q],
+                                           sm.qshift[q], sm.hist + 256 * q);
+            if ((tid & 31) == 0) sm.qresult[q] = kval(r);
+        }
     }
+    __syncthreads();
 }
 
 __device__ void block_select(const double* __restrict__ vals, int64_t n, bool have_range, double vmin, double vmax,
@@ -326,7 +393,7 @@ __device__ void block_select(const double* __restrict__ vals, int64_t n, bool ha
     };
     if (small) {
         // one read into shared memory; the range comes with it
-        for (int64_t i = tid; i < n; i += kSelThreads) {
+        for (int64_t i = tid; i < n; i += blockDim.x) {
             const uint64_t k = okey(vals[i]);
             sm.cand[i] = k;
             minmax(k);
@@ -355,22 +422,227 @@ __device__ void block_select(const double* __restrict__ vals, int64_t n, bool ha
         __syncthreads();
         if (kmin != kmax) {
             const int sh0 = bitlen64(kmax - kmin);
-            for (int q = 0; q < nq; ++q) {
-                const uint64_t r = smem_select(sm.cand, static_cast<int>(n), ranks[q], kmin, sh0, sm);
-                if (tid == 0) sm.qresult[q] = kval(r);
-                __syncthreads();
+            const int q = tid >> 5;
+            if (q < nq) {
+                const uint64_t r = warp_select(sm.cand, static_cast<int>(n), ranks[q], kmin, sh0, sm.hist + 256 * q);
+                if ((tid & 31) == 0) sm.qresult[q] = kval(r);
             }
+            __syncthreads();
         }
     } else {
-        select_in([&](auto&& f) { stream_keys(vals, n, f); }, n, kmin, kmax, ranks, nq, sm);
+        select_in(GlobalSrc{vals, n}, n, kmin, kmax, ranks, nq, sm);
     }
     __syncthreads();
     if (tid < nq) out[tid] = sm.qresult[tid];
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Cluster form (the per-wave summary select): ONE HBM pass.  A 4-CTA thread-block cluster owns a
+// segment; each CTA pulls its quarter into shared memory with a single TMA bulk copy
+// (cp.async.bulk, completion on an mbarrier), builds the 12-bit (key - kmin) >> shift histogram
+// of its quarter there, and adds it into the leader CTA's histogram through distributed shared
+// memory.  The leader locates the bins holding the target ranks; every CTA then copies its
+// in-bin keys from its own shared memory into the leader's candidate buffer (DSMEM atomics +
+// stores), and the leader finishes each quantile with one warp.  Segments of at most one chunk
+// are handled by the leader alone; segments whose target bins overflow the candidate buffer
+// (heavy ties) take the two-pass global path above.
+namespace cg = cooperative_groups;
+
+constexpr int kCS = 4;          // CTAs per cluster
+constexpr int kChunk = 9216;    // doubles per CTA (72 KB of shared memory)
+constexpr int kCCand = 2048;    // leader's candidate keys
+constexpr int kClThreads = 512;
+
+struct ClSmem {
+    double data[kChunk];
+    uint32_t hist[kBins];
+    uint64_t cand[kCCand];
+    unsigned long long mbar;
+    int32_t mode;  // 0: gather + finish, 1: two-pass fallback on the leader
+    int32_t ng;
+    uint32_t gbin[kMaxQ], gbase[kMaxQ], gfill[kMaxQ], gcnt[kMaxQ];
+    int32_t qg[kMaxQ];
+    int64_t qrank[kMaxQ];
+    uint32_t wsum[32];
+};
+static_assert(sizeof(SelSmem) <= sizeof(ClSmem), "fallback reuses the cluster layout");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    }
+}
+
+// f(key) over the first `len` doubles of shared memory, 16-B loads
+template <class F>
+__device__ __forceinline__ void smem_keys(const double* data, int len, F&& f) {
+    const double2* d2 = reinterpret_cast<const double2*>(data);
+    const int n2 = len >> 1;
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const double2 x = d2[i];
+        f(okey(x.x));
+        f(okey(x.y));
+    }
+    if ((len & 1) && threadIdx.x == 0) f(okey(data[len - 1]));
+}
+
+__device__ void cluster_select(const double* __restrict__ vals, int64_t n, double vmin, double vmax, const double* qs,
+                               int nq, double* out, ClSmem& sm) {
+    cg::cluster_group cl = cg::this_cluster();
+    const unsigned crank = cl.block_rank();
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const uint64_t kmin = okey(vmin), kmax = okey(vmax);
+    const int sh0 = bitlen64(kmax - kmin);
+    const bool aligned = (reinterpret_cast<uintptr_t>(vals) & 15) == 0;
+    if (n <= 0 || sh0 == 0 || n > static_cast<int64_t>(kCS) * (kChunk - 2) || !aligned) {
+        if (crank == 0)  // trivial or out-of-range segment: the leader alone, global path
+            block_select(vals, n, true, vmin, vmax, qs, nq, out, *reinterpret_cast<SelSmem*>(&sm));
+        return;
+    }
+    const bool solo = n <= kChunk;
+    if (solo && crank != 0) return;
+    const int parts = solo ? 1 : kCS;
+    const int me = solo ? 0 : static_cast<int>(crank);
+    const int64_t per = ((n + parts - 1) / parts + 1) & ~1ll;
+    const int64_t beg = me * per < n ? me * per : n;
+    const int64_t end = (me + 1) * per < n ? (me + 1) * per : n;
+    const int len = static_cast<int>(end - beg);
+    const int len2 = len & ~1;
+    const int d = sh0 < kDigit ? sh0 : kDigit;
+    const int s1 = sh0 - d;
+    // 1. one bulk copy of this CTA's share (16-B aligned, even length) + the odd tail element
+    if (tid == 0) {
+        mbar_init(&sm.mbar);
+        if (len2 > 0) tma_load_1d(sm.data, vals + beg, static_cast<uint32_t>(len2) * 8u, &sm.mbar);
+        if (len & 1) sm.data[len - 1] = vals[beg + len - 1];
+    }
+    for (int b = tid; b < kBins; b += nthr) sm.hist[b] = 0;
+    if (tid < kMaxQ) sm.gfill[tid] = 0;
+    __syncthreads();
+    if (len2 > 0) mbar_wait(&sm.mbar, 0);
+    // 2. local histogram of (key - kmin) >> s1
+    smem_keys(sm.data, len, [&](uint64_t k) { atomicAdd(&sm.hist[static_cast<uint32_t>((k - kmin) >> s1)], 1u); });
+    __syncthreads();
+    if (!solo) cl.sync();  // (B) every local histogram is complete
+    // 3. the leader folds the other CTAs' histograms into its own (DSMEM reads, all loads of a
+    //    thread independent), locates the target bins and publishes the decisions
+    if (crank == 0) {
+        if (!solo) {
+            const uint32_t* hs[kCS - 1];
+            for (int c = 1; c < kCS; ++c) hs[c - 1] = cl.map_shared_rank(sm.hist, c);
+            for (int b = tid; b < kBins; b += nthr) {
+                uint32_t v0 = hs[0][b], v1 = hs[1][b], v2 = hs[2][b];
+                sm.hist[b] += v0 + v1 + v2;
+            }
+            __syncthreads();
+        }
+        int64_t ranks[kMaxQ];
+        for (int q = 0; q < nq; ++q) {
+            int64_t r = static_cast<int64_t>(ceil(__dmul_rn(qs[q], static_cast<double>(n))));
+            ranks[q] = (r < 1 ? 1 : r > n ? n : r) - 1;
+        }
+        const int per_t = kBins / nthr;
+        uint32_t cnt = 0;
+        for (int b = 0; b < per_t; ++b) cnt += sm.hist[tid * per_t + b];
+        const int64_t below = block_excl_scan(cnt, sm.wsum);
+        for (int q = 0; q < nq; ++q) {
+            const int64_t rk = ranks[q];
+            if (rk >= below && rk < below + cnt) {
+                int64_t acc = below;
+                int bin = tid * per_t;
+                while (acc + sm.hist[bin] <= rk) acc += sm.hist[bin++];
+                sm.qrank[q] = rk - acc;
+                sm.gbin[q] = static_cast<uint32_t>(bin);  // per quantile; deduplicated below
+                sm.gcnt[q] = sm.hist[bin];
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int ng = 0;
+            uint32_t total = 0;
+            uint32_t qb[kMaxQ], qc[kMaxQ];
+            for (int q = 0; q < nq; ++q) {
+                qb[q] = sm.gbin[q];
+                qc[q] = sm.gcnt[q];
+            }
+            for (int q = 0; q < nq; ++q) {
+                int g = -1;
+                for (int p = 0; p < ng; ++p)
+                    if (sm.gbin[p] == qb[q]) g = p;
+                if (g < 0) {
+                    g = ng++;
+                    sm.gbin[g] = qb[q];
+                    sm.gcnt[g] = qc[q];
+                    sm.gbase[g] = total;
+                    total += qc[q];
+                }
+                sm.qg[q] = g;
+            }
+            for (int g = ng; g < kMaxQ; ++g) sm.gbin[g] = 0xffffffffu;
+            sm.ng = ng;
+            sm.mode = total <= static_cast<uint32_t>(kCCand) ? 0 : 1;
+        }
+        __syncthreads();
+    }
+    if (!solo) cl.sync();  // (C) decisions visible cluster-wide
+    ClSmem& L = solo ? sm : *cl.map_shared_rank(&sm, 0);
+    const int mode = L.mode;
+    if (mode == 0) {
+        // 4. every CTA copies its in-bin keys from its own shared memory to the leader's buffer
+        uint32_t gb[kMaxQ], gbase[kMaxQ];
+        for (int g = 0; g < kMaxQ; ++g) {
+            gb[g] = L.gbin[g];
+            gbase[g] = L.gbase[g];
+        }
+        smem_keys(sm.data, len, [&](uint64_t k) {
+            const uint32_t dg = static_cast<uint32_t>((k - kmin) >> s1);
+#pragma unroll
+            for (int g = 0; g < kMaxQ; ++g)
+                if (dg == gb[g]) {
+                    const uint32_t at = atomicAdd(&L.gfill[g], 1u);
+                    L.cand[gbase[g] + at] = k;
+                }
+        });
+    }
+    if (!solo) cl.sync();  // (D) candidates complete and no CTA reads a remote histogram any more
+    if (crank != 0) return;
+    if (mode == 1) {
+        block_select(vals, n, true, vmin, vmax, qs, nq, out, *reinterpret_cast<SelSmem*>(&sm));
+        return;
+    }
+    __syncthreads();
+    const int q = tid >> 5;  // warp q finishes quantile q
+    if (q < nq) {
+        const int g = sm.qg[q];
+        const uint64_t r = warp_select(sm.cand + sm.gbase[g], static_cast<int>(sm.gcnt[g]), sm.qrank[q],
+                                       kmin + (static_cast<uint64_t>(sm.gbin[g]) << s1), s1, sm.hist + 256 * q);
+        if ((tid & 31) == 0) out[q] = kval(r);
+    }
+}
 }  // namespace
 
-__global__ void __launch_bounds__(kSelThreads) select_kernel(WaveBuffers B, int T, int n_rep) {
+__global__ void __launch_bounds__(kSelThreads, 4) select_kernel(WaveBuffers B, int T, int n_rep) {
     extern __shared__ __align__(16) unsigned char smem[];
     SelSmem& sm = *reinterpret_cast<SelSmem*>(smem);
     const int s = blockIdx.x;
@@ -385,7 +657,7 @@ __global__ void __launch_bounds__(kSelThreads) select_kernel(WaveBuffers B, int 
                  true, o.win_min, o.win_max, qs, kMaxQ, B.quant + 4ll * so, sm);
 }
 
-__global__ void __launch_bounds__(kSelThreads) select_segments_kernel(const double* __restrict__ vals,
+__global__ void __launch_bounds__(kSelThreads, 4) select_segments_kernel(const double* __restrict__ vals,
                                                                       const int64_t* __restrict__ seg_off, int n_seg,
                                                                       const double* __restrict__ qs, int nq,
                                                                       double* __restrict__ out) {
@@ -401,6 +673,24 @@ __global__ void __launch_bounds__(kSelThreads) select_segments_kernel(const doub
     }
 }
 
+__global__ void __cluster_dims__(kCS, 1, 1) __launch_bounds__(kClThreads, 2)
+    select_cluster_kernel(WaveBuffers B, int T, int n_rep) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    ClSmem& sm = *reinterpret_cast<ClSmem*>(smem);
+    const int s = blockIdx.x / kCS;  // one cluster per segment
+    if (s >= n_rep * T) return;
+    const int r = s % n_rep, t = B.sel_order[s / n_rep];
+    const int so = r * T + t;
+    const TenantOut& o = B.tout[so];
+    const double qs[kMaxQ] = {0.50, 0.95, 0.99, 0.999};
+    cluster_select(B.win_lat + static_cast<int64_t>(r) * B.cap_sum + B.off[t], static_cast<int64_t>(o.completed_window),
+                   o.win_min, o.win_max, qs, kMaxQ, B.quant + 4ll * so, sm);
+}
+
 size_t select_smem_bytes() { return sizeof(SelSmem); }
+size_t select_cluster_smem_bytes() { return sizeof(ClSmem); }
+int select_cluster_size() { return kCS; }
+int select_cluster_threads() { return kClThreads; }
+int select_threads() { return kSelThreads; }
 
 }  // namespace mg

@@ -102,3 +102,25 @@ def test_select_many_segments_shared_groups(engine):
         for q, v in zip(qs, row):
             r = min(max(int(np.ceil(q * n)), 1), n) - 1
             assert v == srt[r], (n, q, v, srt[r])
+
+
+def test_cluster_select_matches_two_pass(engine, monkeypatch):
+    """The one-HBM-pass cluster select (MIGSIM_SELECT=cluster: TMA bulk loads, DSMEM histogram and
+    gather) returns exactly the two-pass kernel's p50/p95/p99/p999 on every segment of a wave."""
+    import os
+
+    from tests._libs import CONFIG_DIR
+
+    path = os.path.join(CONFIG_DIR, "c2_cluster16.yaml")
+    sid = engine.load_scenario(path)
+    seeds = list(range(1, 17))
+    a = engine.run_batch(sid, seeds)
+    monkeypatch.setenv("MIGSIM_SELECT", "cluster")
+    b = engine.run_batch(sid, seeds)
+    try:
+        for k in ("p50_ms", "p95_ms", "p99_ms", "p999_ms"):
+            assert (a.rows[k].view(np.uint64) == b.rows[k].view(np.uint64)).all(), k
+        assert (a.rows["completed_window"] == b.rows["completed_window"]).all()
+    finally:
+        a.close()
+        b.close()

@@ -12,6 +12,6 @@ import json; d=json.load(open('gpurun_out/bench.json')); print('VALUE', d['value
 fi
 NCU=/usr/local/cuda/bin/ncu
 [ -z "$NO_LAUNCHES" ] && timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --c4-seeds 0 > gpurun_out/bench_under_ncu.txt 2>&1
-[ -z "$NO_SEL_NCU" ] && timeout 300 $NCU --set full --clock-control none --import-source on -k regex:"select_kernel" -c 1 -o gpurun_out/prof_select python tools/prof_one.py 256 > gpurun_out/prof_select.txt 2>&1
+[ -z "$NO_SEL_NCU" ] && timeout 300 $NCU --set full --clock-control none --import-source on -k regex:"select" -c 1 -o gpurun_out/prof_select python tools/prof_one.py 256 > gpurun_out/prof_select.txt 2>&1
 [ -z "$NO_DES_NCU" ] && timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"des_kernel" -c 1 -o gpurun_out/prof_des python tools/prof_one.py 256 > gpurun_out/prof_des.txt 2>&1
 ls gpurun_out

@@ -153,6 +153,7 @@ def load_library() -> ctypes.CDLL:
     lib.migsim_render_report.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
     lib.migsim_gpu_admit.argtypes = [vp, ctypes.c_int32, sz] + [vp] * 11 + [ctypes.POINTER(ctypes.c_double), cp, sz]
     lib.migsim_free.argtypes = [vp]
+    lib.migsim_scenario_dump.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
     _lib_handle = lib
     return lib
 
@@ -419,6 +420,19 @@ def run_plan(plan: str, scenario_path: str, seeds: int = 7, seed_base: int = 1, 
              out_dir: str = "") -> dict:
     """harness::run_plan (harness.cpp:114-216) with the replica fan-out as one GPU batch."""
     return default_engine().run_plan(plan, scenario_path, seeds, seed_base, focus_tenant, out_dir)
+
+
+def scenario_spec(path: str) -> dict:
+    """The scenario-v1 file as the engine's loader normalises it (presets applied, file order of
+    tenants kept): scenario::load_scenario (scenario.cpp:376-384)."""
+    lib = load_library()
+    out = ctypes.c_void_p()
+    err = ctypes.create_string_buffer(1024)
+    _check(lib.migsim_scenario_dump(path.encode(), ctypes.byref(out), err, 1024), err)
+    try:
+        return json.loads(ctypes.string_at(out.value).decode())
+    finally:
+        lib.migsim_free(out)
 
 
 def render_report(experiment: "dict | str") -> str:

@@ -223,7 +223,7 @@ struct TenantCtl {
     int32_t vn;
     int32_t breach_windows, next_rung, acted_ever, backfired, none_logged, relax_blocked, validating, drain_seen;
     int32_t action_seq, prior_host, prior_gpu, prior_first, prior_count, prior_profile, ema_has, ema_trig;
-    uint64_t obs_in_window, obs_since_action, relax_run, obs_total;
+    uint32_t obs_in_window, obs_since_action, relax_run, obs_total;  // 32-bit: < 2^32 per run
     double window_end_s, ignore_before_s, validation_start_s, pre_p99_ms, ema, trigger, clear;
     int32_t app_kind, app_target, app_diag, pad;
 };
@@ -236,7 +236,7 @@ struct TenantDyn {
     double remaining, started_s, transfer_ms, last_settle, grant;
     double compute_done_ms, svc_ms, extra_ms, compute_end, cur_transfer_ms;
     double pend_pause;
-    uint64_t completed, n_window, misses;
+    uint32_t completed, n_window, misses, pad_c;  // 32-bit counters (widened in finish)
     double sum_total;
     double win_min, win_max;
     int64_t base;   // offset of this tenant's records inside the replica's arrays
@@ -344,7 +344,7 @@ struct Sim {
     int T;
     // per-event scalars kept out of shared memory (registers once inlined into the kernel)
     double now;
-    uint64_t next_seq, n_events;
+    uint32_t next_seq, n_events;  // seq < 2^29 is checked in finish
     Mask live_resume, live_expire;  // tenants with a live resume / guardrail-expire event
     // Working-set arrays held as registers (not re-loaded from SimState) so that, after inlining
     // into the kernel, the compiler sees shared-memory provenance and emits LDS/STS.
@@ -392,7 +392,7 @@ struct Sim {
 
     MG_HD void push(int kind, int i, double t) {
         if (rare_kind(kind)) mark_rare(kind, i, true);
-        lanes.set(slot_index(kind, i), t, (static_cast<uint64_t>(kind) << 48) | next_seq);
+        lanes.set(slot_index(kind, i), t, (static_cast<uint64_t>(kind) << 48) | static_cast<uint64_t>(next_seq));
         next_seq += 1;
     }
     MG_HD void cancel(int kind, int i) {
@@ -1374,7 +1374,7 @@ struct Sim {
         if (t < C.warmup_s) return no_action();
         uint64_t required = static_cast<uint64_t>(C.dwell_obs);
         if (c.backfired) required += static_cast<uint64_t>(C.cooldown_obs);
-        const bool gates = !c.acted_ever || c.obs_since_action >= required;
+        const bool gates = !c.acted_ever || static_cast<uint64_t>(c.obs_since_action) >= required;
         const bool eligible = spec(i).tclass == kLatencySensitive;
         if (eligible && c.breach_windows >= C.persistence_windows && gates) {
             Action act = evaluate_breach(i, c);
@@ -1389,7 +1389,7 @@ struct Sim {
             }
             return no_action();
         }
-        if (C.enable_mig && gates && c.relax_run >= static_cast<uint64_t>(C.dwell_obs) && !c.ema_trig) {
+        if (C.enable_mig && gates && static_cast<uint64_t>(c.relax_run) >= static_cast<uint64_t>(C.dwell_obs) && !c.ema_trig) {
             Action act = try_relax(i, c);
             if (act.valid) {
                 adopt(i, c, act, p99, t);
@@ -1454,7 +1454,7 @@ struct Sim {
             d.started_s = -1.0;
             d.compute_done_ms = d.svc_ms = d.extra_ms = d.compute_end = d.cur_transfer_ms = 0.0;
             d.pend_pause = 0.0;
-            d.completed = d.n_window = d.misses = 0;
+            d.completed = d.n_window = d.misses = d.pad_c = 0;
             d.sum_total = 0.0;
             d.win_min = k_inf();
             d.win_max = -k_inf();
@@ -1538,7 +1538,7 @@ struct Sim {
         io.rout->n_actions = st.n_actions;
         io.rout->n_pauses = st.n_pauses;
         // the device event order packs seq into 29 bits (engine_kernels.cu); never silently wrap
-        io.rout->error = next_seq >= (1ull << 29) ? kErrSeqOverflow : st.error;
+        io.rout->error = next_seq >= (1u << 29) ? kErrSeqOverflow : st.error;
         io.rout->pad = 0;
         io.rout->n_events = n_events;
     }

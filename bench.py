@@ -280,7 +280,7 @@ def run_engine(args):
                    "(per-step arrival records ~5 GB regenerated on device each step)"},
         "e2e": {"value": ticks / wall_s, "unit": "tenant-ticks/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
-        "roofline": {"bound": "hbm", "kernel": "des_kernel", "achieved": des_gbs, "peak": hbm, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": "des_kernel_reg" if T <= 10 else "des_kernel", "achieved": des_gbs, "peak": hbm, "unit": "GB/s",
                      "frac": des_gbs / hbm, "traffic": traffic, "peak_kind": peak_kind,
                      "note": "replica DES is latency/issue bound (one sequential event loop per warp); "
                              "48 B algorithmic per completion"},

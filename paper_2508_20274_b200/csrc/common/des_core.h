@@ -27,6 +27,7 @@
 
 #include "arrivals.h"
 #include "des_types.h"
+#include "lat_hist.h"
 #include "packed.h"
 
 #if defined(__CUDA_ARCH__)
@@ -61,6 +62,7 @@ struct ReplicaIO {
     uint64_t* mt_pause;       // n_tenants * 312
     // outputs
     double* win_lat;          // measurement-window latencies, same offsets
+    uint32_t* win_hist;       // optional [T][kHistBins] histogram of the same latencies (lat_hist.h)
     ActionRec* actions;
     int32_t action_cap;
     PauseRec* pauses;
@@ -250,6 +252,15 @@ MG_HD int __popcll_hd(uint64_t m) {
     return __popcll(static_cast<unsigned long long>(m));
 #else
     return __builtin_popcountll(m);
+#endif
+}
+
+MG_HD void hist_add(uint32_t* p) {
+#if defined(__CUDA_ARCH__)
+    // the handlers run warp-uniformly (every lane executes them): one lane counts
+    if ((threadIdx.x & 31) == 0) atomicAdd(p, 1u);  // result unused: a fire-and-forget RED
+#else
+    *p += 1;
 #endif
 }
 
@@ -685,6 +696,7 @@ struct Sim {
             if (total < d.win_min) d.win_min = total;
             if (total > d.win_max) d.win_max = total;
             if (total > spec(i).slo_tail_ms) d.misses += 1;
+            if (io.win_hist) hist_add(io.win_hist + static_cast<int64_t>(i) * kHistBins + lat_bin(total));
         }
         if (io.c_total) {
             const int64_t o = base + static_cast<int64_t>(idx);

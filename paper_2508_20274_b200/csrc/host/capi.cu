@@ -73,24 +73,62 @@ int guarded(char* err, size_t errlen, F&& f) {
 template <class T>
 struct DevBuf {
     T* p = nullptr;
-    size_t n = 0;
+    size_t n = 0, cap = 0;
+    // keeps an existing allocation when it is large enough (wave buffers persist across batches
+    // of a handle, so repeated batches do no cudaMalloc/cudaFree)
     void alloc(size_t count) {
+        n = count;
+        if (p && count <= cap) return;
         free();
         n = count;
         if (count) CK(cudaMalloc(&p, sizeof(T) * count));
+        cap = count;
     }
     void free() {
         if (p) cudaFree(p);
         p = nullptr;
-        n = 0;
+        n = cap = 0;
     }
+    size_t bytes() const { return sizeof(T) * cap; }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { free(); }
+};
+
+
+struct WaveAlloc {
+    DevBuf<double> arr_t, arr_bytes, arr_mult, arr_noise, irq_e, t_all, req_ms, win_lat;
+    DevBuf<double> c_done, c_total, c_compute, c_transfer, c_noise;
+    DevBuf<int32_t> n_all, n_kept, variant, gen_overflow, file_order, sel_order;
+    DevBuf<uint64_t> mt_pause, seeds;
+    DevBuf<mg::ActionRec> actions, actions_c;
+    DevBuf<mg::PauseRec> pauses, pauses_c;
+    DevBuf<mg::TenantOut> tout;
+    DevBuf<mg::ReplicaOut> rout;
+    DevBuf<double> backlog, quant, rings;
+    DevBuf<int64_t> off, cap, act_off, pause_off, c_order;
+    DevBuf<mg::CounterRow> tr_cnt;
+    DevBuf<mg::FabricRow> tr_fab;
+    DevBuf<mg::TailWin> tr_win;
+    DevBuf<uint32_t> win_hist;
+    DevBuf<double> tr_ring;
+    DevBuf<mg::PScenario> scen;
+    DevBuf<mg::PController> ctrl;
+    size_t bytes() const {
+        return arr_t.bytes() + arr_bytes.bytes() + arr_mult.bytes() + arr_noise.bytes() + irq_e.bytes() + t_all.bytes() +
+               req_ms.bytes() + win_lat.bytes() + c_done.bytes() + c_total.bytes() + c_compute.bytes() +
+               c_transfer.bytes() + c_noise.bytes() + mt_pause.bytes() + actions.bytes() + actions_c.bytes() +
+               pauses.bytes() + pauses_c.bytes() + rings.bytes() + win_hist.bytes() + c_order.bytes() + tr_cnt.bytes() +
+               tr_fab.bytes() + tr_ring.bytes();
+    }
 };
 
 }  // namespace
 
 struct migsim_gpu {
     int device = 0;
+    WaveAlloc wave;  // device buffers of the last batch, reused by the next
     cudaStream_t stream = nullptr;
     cudaEvent_t ev[6] = {};
     std::vector<mgb::ScenarioSpec> scenarios;
@@ -120,24 +158,7 @@ struct migsim_batch_result {
 
 namespace {
 
-struct WaveAlloc {
-    DevBuf<double> arr_t, arr_bytes, arr_mult, arr_noise, irq_e, t_all, req_ms, win_lat;
-    DevBuf<double> c_done, c_total, c_compute, c_transfer, c_noise;
-    DevBuf<int32_t> n_all, n_kept, variant, gen_overflow, file_order, sel_order;
-    DevBuf<uint64_t> mt_pause, seeds;
-    DevBuf<mg::ActionRec> actions, actions_c;
-    DevBuf<mg::PauseRec> pauses, pauses_c;
-    DevBuf<mg::TenantOut> tout;
-    DevBuf<mg::ReplicaOut> rout;
-    DevBuf<double> backlog, quant, rings;
-    DevBuf<int64_t> off, cap, act_off, pause_off, c_order;
-    DevBuf<mg::CounterRow> tr_cnt;
-    DevBuf<mg::FabricRow> tr_fab;
-    DevBuf<mg::TailWin> tr_win;
-    DevBuf<double> tr_ring;
-    DevBuf<mg::PScenario> scen;
-    DevBuf<mg::PController> ctrl;
-};
+
 
 void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vector<mgb::Variant>& variants,
                     const std::vector<uint64_t>& seeds, const migsim_run_opts& opts, migsim_batch_result& res,
@@ -167,15 +188,17 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
                            static_cast<size_t>(T) * mg::kMtN * 8 + static_cast<size_t>(action_cap) * sizeof(mg::ActionRec) * 2 +
                            static_cast<size_t>(pause_cap) * sizeof(mg::PauseRec) * 2 + T * sizeof(mg::TenantOut) +
                            sizeof(mg::ReplicaOut) + static_cast<size_t>(R) * 16 + static_cast<size_t>(T) * 32 + 64 +
+                           static_cast<size_t>(T) * mg::kHistBins * 4 +
                            (rings_in_smem ? 0 : static_cast<size_t>(T) * (P.max_dwell + P.max_validation) * 8);
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
+    free_b += g->wave.bytes();  // the handle's cached wave buffers are reusable
     size_t W = std::max<size_t>(1, static_cast<size_t>(0.70 * static_cast<double>(free_b)) / per_rep);
     if (opts.max_wave_replicas > 0) W = std::min<size_t>(W, static_cast<size_t>(opts.max_wave_replicas));
     W = std::min(W, n_jobs);
     if (W == 0) W = 1;
 
-    WaveAlloc A;
+    WaveAlloc& A = g->wave;
     const size_t big = W * static_cast<size_t>(P.cap_sum);
     A.arr_t.alloc(big);
     A.arr_bytes.alloc(big);
@@ -185,6 +208,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     A.t_all.alloc(big);
     A.req_ms.alloc(big);
     A.win_lat.alloc(big);
+    A.win_hist.alloc(W * T * mg::kHistBins);
     if (keep) {
         A.c_done.alloc(big);
         A.c_total.alloc(big);
@@ -252,15 +276,17 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     B.t_all = A.t_all.p;
     B.req_ms = A.req_ms.p;
     B.win_lat = A.win_lat.p;
-    B.c_done = A.c_done.p;
-    B.c_total = A.c_total.p;
-    B.c_compute = A.c_compute.p;
-    B.c_transfer = A.c_transfer.p;
-    B.c_noise = A.c_noise.p;
-    B.c_order = A.c_order.p;
-    B.tr_cnt = A.tr_cnt.p;
-    B.tr_fab = A.tr_fab.p;
-    B.tr_win = A.tr_win.p;
+    B.win_hist = A.win_hist.p;
+    // optional streams: only when this batch asks for them (the cached buffers may hold others)
+    B.c_done = keep ? A.c_done.p : nullptr;
+    B.c_total = keep ? A.c_total.p : nullptr;
+    B.c_compute = keep ? A.c_compute.p : nullptr;
+    B.c_transfer = keep ? A.c_transfer.p : nullptr;
+    B.c_noise = keep ? A.c_noise.p : nullptr;
+    B.c_order = keep ? A.c_order.p : nullptr;
+    B.tr_cnt = traces ? A.tr_cnt.p : nullptr;
+    B.tr_fab = traces ? A.tr_fab.p : nullptr;
+    B.tr_win = traces ? A.tr_win.p : nullptr;
     B.n_all = A.n_all.p;
     B.n_kept = A.n_kept.p;
     B.mt_pause = A.mt_pause.p;
@@ -270,7 +296,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     B.rout = A.rout.p;
     B.backlog = A.backlog.p;
     B.quant = A.quant.p;
-    B.rings = A.rings.p;
+    B.rings = rings_in_smem ? nullptr : A.rings.p;
     B.seeds = A.seeds.p;
     B.variant = A.variant.p;
     B.off = A.off.p;
@@ -303,6 +329,8 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     // C2 wave, 0.24 vs 0.15 ms -- DESIGN.md section 6)
     const char* sel_env = std::getenv("MIGSIM_SELECT");
     const bool sel_cluster = sel_env && std::string(sel_env) == "cluster";
+    // MIGSIM_SELECT=two-pass: ignore the producer histogram (the two-pass digit select)
+    const bool sel_two_pass = sel_env && std::string(sel_env) == "two-pass";
 
     res.tout.resize(n_jobs * T);
     res.quant.resize(n_jobs * T * 4);
@@ -329,6 +357,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         CK(cudaMemcpyAsync(A.variant.p, wvar.data(), sizeof(int32_t) * w, cudaMemcpyHostToDevice, s));
         CK(cudaMemsetAsync(A.gen_overflow.p, 0, sizeof(int32_t), s));
         CK(cudaEventRecord(g->ev[0], s));
+        CK(cudaMemsetAsync(A.win_hist.p, 0, sizeof(uint32_t) * w * T * mg::kHistBins, s));  // timed with gen
         const int64_t nt = static_cast<int64_t>(w) * T;
         mg::gen_times_kernel<<<static_cast<unsigned>(nt), 32, mg::gen_times_smem_bytes(), s>>>(A.scen.p, B, w);
         mg::gen_marks_kernel<<<static_cast<unsigned>(4 * nt), 32, 0, s>>>(A.scen.p, B, w);
@@ -340,8 +369,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         if (sel_cluster)
             mg::select_cluster_kernel<<<static_cast<unsigned>(nt * mg::select_cluster_size()), mg::select_cluster_threads(),
                                         cl_smem, s>>>(B, T, w);
-        else
-            mg::select_kernel<<<static_cast<unsigned>(nt), mg::select_threads(), sel_smem, s>>>(B, T, w);
+        else {
+            mg::WaveBuffers Bs = B;
+            if (sel_two_pass) Bs.win_hist = nullptr;
+            mg::select_kernel<<<static_cast<unsigned>(nt), mg::select_threads(), sel_smem, s>>>(Bs, T, w);
+        }
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[3], s));
         int32_t overflow = 0;

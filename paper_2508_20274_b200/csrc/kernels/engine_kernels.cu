@@ -231,6 +231,7 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
     io.req_transfer_ms = B.req_ms + base;
     io.mt_pause = B.mt_pause + static_cast<int64_t>(r) * T * kMtN;
     io.win_lat = B.win_lat + base;
+    io.win_hist = B.win_hist ? B.win_hist + static_cast<int64_t>(r) * T * kHistBins : nullptr;
     io.actions = B.actions + static_cast<int64_t>(r) * B.action_cap;
     io.action_cap = B.action_cap;
     io.pauses = B.pauses + static_cast<int64_t>(r) * B.pause_cap;

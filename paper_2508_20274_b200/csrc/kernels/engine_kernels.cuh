@@ -23,6 +23,7 @@ struct WaveBuffers {
     double *arr_t, *arr_bytes, *arr_mult, *arr_noise, *irq_e, *t_all, *req_ms, *win_lat;
     double *c_done, *c_total, *c_compute, *c_transfer, *c_noise;  // optional
     int64_t* c_order;                                              // optional, [W][cap_sum]
+    uint32_t* win_hist;                                            // [W][T][kHistBins] window-latency bins
     CounterRow* tr_cnt;                                            // optional traces [W][n_ticks][T]
     FabricRow* tr_fab;                                             //                 [W][n_ticks][R]
     TailWin* tr_win;                                               //                 [W][T]

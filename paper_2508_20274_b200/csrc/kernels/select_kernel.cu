@@ -437,6 +437,105 @@ __device__ void block_select(const double* __restrict__ vals, int64_t n, bool ha
 }
 
 
+// Producer-histogram form (the default for the per-wave summary): the DES already binned every
+// window latency (lat_hist.h), so the target bins are known before the samples are touched and ONE
+// streaming pass over HBM gathers the in-bin keys; one warp per quantile finishes.  Falls back to
+// the two-pass path when the target bins hold more keys than the gather buffer.
+__device__ void hist_select(const double* __restrict__ vals, int64_t n, const uint32_t* __restrict__ hist,
+                            double vmin, double vmax, const double* qs, int nq, double* out, SelSmem& sm) {
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    const uint64_t kmin = okey(vmin), kmax = okey(vmax);
+    if (n <= kCand || kmin == kmax) {  // small or constant segments: the shared-memory path
+        block_select(vals, n, true, vmin, vmax, qs, nq, out, sm);
+        return;
+    }
+    int64_t ranks[kMaxQ];
+    for (int q = 0; q < nq; ++q) {
+        int64_t r = static_cast<int64_t>(ceil(__dmul_rn(qs[q], static_cast<double>(n))));
+        ranks[q] = (r < 1 ? 1 : r > n ? n : r) - 1;
+    }
+    // histogram -> smem (coalesced 16-B loads), locate the rank bins
+    {
+        const uint4* h4 = reinterpret_cast<const uint4*>(hist);
+        uint4* s4 = reinterpret_cast<uint4*>(sm.hist);
+        for (int i = tid; i < kHistBins / 4; i += nthr) s4[i] = __ldg(h4 + i);
+    }
+    __syncthreads();
+    const int per = kHistBins / nthr;
+    uint32_t cnt = 0;
+    for (int b = 0; b < per; ++b) cnt += sm.hist[tid * per + b];
+    const int64_t below = block_excl_scan(cnt, sm.wsum);
+    for (int q = 0; q < nq; ++q) {
+        const int64_t rk = ranks[q];
+        if (rk >= below && rk < below + cnt) {
+            int64_t acc = below;
+            int bin = tid * per;
+            while (acc + sm.hist[bin] <= rk) acc += sm.hist[bin++];
+            sm.qrank[q] = rk - acc;
+            sm.qlo[q] = static_cast<uint64_t>(bin);  // bin index for now
+            sm.qgroup[q] = sm.hist[bin];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {  // distinct bins -> slices of the candidate buffer
+        uint32_t total = 0;
+        for (int q = 0; q < nq; ++q) {
+            sm.qslot[q] = q;
+            for (int p = 0; p < q; ++p)
+                if (sm.qlo[p] == sm.qlo[q]) {
+                    sm.qslot[q] = sm.qslot[p];
+                    break;
+                }
+            if (sm.qslot[q] == q) {
+                sm.qbase[q] = total;
+                sm.qfill[q] = 0;
+                total += static_cast<uint32_t>(sm.qgroup[q]);
+            }
+        }
+        sm.fits = total <= static_cast<uint32_t>(kCand);
+    }
+    __syncthreads();
+    if (!sm.fits) {
+        __syncthreads();
+        block_select(vals, n, true, vmin, vmax, qs, nq, out, sm);
+        return;
+    }
+    uint32_t gb[kMaxQ];
+    int gq[kMaxQ];
+    for (int g = 0; g < kMaxQ; ++g) {
+        const bool own = g < nq && sm.qslot[g] == g;
+        gb[g] = own ? static_cast<uint32_t>(sm.qlo[g]) : 0xffffffffu;
+        gq[g] = own ? g : 0;
+    }
+    // the one pass over HBM: the gathered keys are the only reuse, so the lines are not kept
+    stream_keys(
+        vals, n,
+        [&](uint64_t k) {
+            const uint32_t b = lat_bin_of_key(k);
+#pragma unroll
+            for (int g = 0; g < kMaxQ; ++g)
+                if (b == gb[g]) {
+                    const uint32_t at = atomicAdd(&sm.qfill[gq[g]], 1u);
+                    sm.cand[sm.qbase[gq[g]] + at] = k;
+                }
+        },
+        false);
+    __syncthreads();
+    const int q = tid >> 5;  // warp q finishes quantile q
+    if (q < nq) {
+        const int o = sm.qslot[q];
+        const uint32_t b = static_cast<uint32_t>(sm.qlo[q]);
+        // interior bins are exact key intervals; the clamped edge bins are bounded by the range
+        const bool interior = b > 0 && b < static_cast<uint32_t>(kHistBins - 1);
+        const uint64_t lo = interior ? lat_bin_lo(b) : kmin;
+        const int sh = interior ? kHistShift : bitlen64(kmax - kmin);
+        const uint64_t r = warp_select(sm.cand + sm.qbase[o], static_cast<int>(sm.qgroup[o]), sm.qrank[q], lo, sh,
+                                       sm.hist + 256 * q);
+        if ((tid & 31) == 0) out[q] = kval(r);
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Cluster form (the per-wave summary select): ONE HBM pass.  A 4-CTA thread-block cluster owns a
 // segment; each CTA pulls its quarter into shared memory with a single TMA bulk copy
@@ -653,8 +752,13 @@ __global__ void __launch_bounds__(kSelThreads, 4) select_kernel(WaveBuffers B, i
     const int so = r * T + t;
     const TenantOut& o = B.tout[so];
     const double qs[kMaxQ] = {0.50, 0.95, 0.99, 0.999};
-    block_select(B.win_lat + static_cast<int64_t>(r) * B.cap_sum + B.off[t], static_cast<int64_t>(o.completed_window),
-                 true, o.win_min, o.win_max, qs, kMaxQ, B.quant + 4ll * so, sm);
+    const double* vals = B.win_lat + static_cast<int64_t>(r) * B.cap_sum + B.off[t];
+    if (B.win_hist)
+        hist_select(vals, static_cast<int64_t>(o.completed_window), B.win_hist + static_cast<int64_t>(so) * kHistBins,
+                    o.win_min, o.win_max, qs, kMaxQ, B.quant + 4ll * so, sm);
+    else
+        block_select(vals, static_cast<int64_t>(o.completed_window), true, o.win_min, o.win_max, qs, kMaxQ,
+                     B.quant + 4ll * so, sm);
 }
 
 __global__ void __launch_bounds__(kSelThreads, 4) select_segments_kernel(const double* __restrict__ vals,

@@ -120,6 +120,7 @@ def hostsim() -> ctypes.CDLL:
         lib.hostsim_arrivals.restype = ctypes.c_long
         lib.hostsim_arrivals.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.c_int, vp, ctypes.c_long]
         lib.hostsim_math.argtypes = [ctypes.c_int, vp, vp, vp, ctypes.c_long]
+        lib.hostsim_lat_bin.argtypes = [vp, vp, vp, vp, ctypes.c_long]
         _hostsim = lib
     return _hostsim
 

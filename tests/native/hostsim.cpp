@@ -264,6 +264,15 @@ long hostsim_arrivals(const char* yaml_path, uint64_t seed, int tenant, double* 
     }
 }
 
+// latency bins shared by the DES and the select kernel (lat_hist.h): bin and the bin's key floor
+void hostsim_lat_bin(const double* x, uint32_t* bin, uint64_t* key, uint64_t* lo, long n) {
+    for (long i = 0; i < n; ++i) {
+        bin[i] = mg::lat_bin(x[i]);
+        key[i] = mg::lat_key(x[i]);
+        lo[i] = mg::lat_bin_lo(bin[i]);
+    }
+}
+
 // glibc-exact math restatement, for the CPU bit-compare test.
 void hostsim_math(int fn, const double* x, const double* y, double* out, long n) {
     for (long i = 0; i < n; ++i)

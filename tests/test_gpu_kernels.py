@@ -104,23 +104,42 @@ def test_select_many_segments_shared_groups(engine):
             assert v == srt[r], (n, q, v, srt[r])
 
 
-def test_cluster_select_matches_two_pass(engine, monkeypatch):
-    """The one-HBM-pass cluster select (MIGSIM_SELECT=cluster: TMA bulk loads, DSMEM histogram and
-    gather) returns exactly the two-pass kernel's p50/p95/p99/p999 on every segment of a wave."""
+@pytest.mark.parametrize("name", ["c2_cluster16.yaml", "default.yaml", "c5_mc64.yaml"])
+def test_select_variants_agree_with_sorted_completions(engine, monkeypatch, name):
+    """All three summary-select paths -- the default producer-histogram one-pass select, the
+    two-pass digit select (MIGSIM_SELECT=two-pass) and the TMA/DSMEM cluster select
+    (MIGSIM_SELECT=cluster) -- return exactly the nearest-rank p50/p95/p99/p999 of the sorted
+    measurement-window latencies (engine.cpp:800-816) for every (replica, tenant)."""
     import os
 
-    from tests._libs import CONFIG_DIR
+    from tests._libs import CONFIG_DIR, SCEN_DIR
 
-    path = os.path.join(CONFIG_DIR, "c2_cluster16.yaml")
+    path = os.path.join(CONFIG_DIR if name.startswith("c") else SCEN_DIR, name)
     sid = engine.load_scenario(path)
-    seeds = list(range(1, 17))
-    a = engine.run_batch(sid, seeds)
-    monkeypatch.setenv("MIGSIM_SELECT", "cluster")
-    b = engine.run_batch(sid, seeds)
+    seeds = list(range(1, 9)) if not name.startswith("c5") else [1, 2]
+    runs = {}
+    for mode in ("default", "two-pass", "cluster"):
+        if mode == "default":
+            monkeypatch.delenv("MIGSIM_SELECT", raising=False)
+        else:
+            monkeypatch.setenv("MIGSIM_SELECT", mode)
+        runs[mode] = engine.run_batch(sid, seeds, keep_completions=(mode == "default"))
+    a = runs["default"]
     try:
-        for k in ("p50_ms", "p95_ms", "p99_ms", "p999_ms"):
-            assert (a.rows[k].view(np.uint64) == b.rows[k].view(np.uint64)).all(), k
-        assert (a.rows["completed_window"] == b.rows["completed_window"]).all()
+        ms = a.run(0)["measure_start_s"]
+        for i in range(len(seeds)):
+            comp = a.completions(i)
+            for t in range(a.n_tenants):
+                v = np.sort(comp[(comp[:, 0] == t) & (comp[:, 2] >= ms), 3])
+                n = len(v)
+                assert n == a.rows[i, t]["completed_window"]
+                for q, k in ((0.5, "p50_ms"), (0.95, "p95_ms"), (0.99, "p99_ms"), (0.999, "p999_ms")):
+                    if n:
+                        r = min(max(int(np.ceil(q * n)), 1), n) - 1
+                        assert a.rows[i, t][k] == v[r], (i, t, k)
+        for mode in ("two-pass", "cluster"):
+            for k in ("p50_ms", "p95_ms", "p99_ms", "p999_ms"):
+                assert (a.rows[k].view(np.uint64) == runs[mode].rows[k].view(np.uint64)).all(), (mode, k)
     finally:
-        a.close()
-        b.close()
+        for r in runs.values():
+            r.close()

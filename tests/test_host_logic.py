@@ -157,3 +157,25 @@ def test_capi_exports_every_declared_symbol():
     from paper_2508_20274_b200.api import EXPORTED_SYMBOLS
 
     assert set(EXPORTED_SYMBOLS) <= declared
+
+
+def test_latency_bins_monotone_and_exact_intervals():
+    """lat_hist.h (DES-side histogram feeding the one-pass select): bins are monotone in the value,
+    clamp at both ends, and an interior bin is exactly the key interval [lat_bin_lo(b), +2^46)."""
+    from tests._libs import hostsim
+
+    rng = np.random.default_rng(4)
+    x = np.concatenate([rng.lognormal(2.0, 2.5, 200_000), [0.0, 1e-300, 2.0 ** -10, np.nextafter(2.0 ** -10, 0),
+                                                           2.0 ** 22, np.nextafter(2.0 ** 22, 0), 1e300, 1.0, 2.0]])
+    x = np.sort(x)
+    n = len(x)
+    b = np.zeros(n, np.uint32)
+    k = np.zeros(n, np.uint64)
+    lo = np.zeros(n, np.uint64)
+    hostsim().hostsim_lat_bin(x.ctypes.data, b.ctypes.data, k.ctypes.data, lo.ctypes.data, n)
+    assert (np.diff(b.astype(np.int64)) >= 0).all()
+    assert b[0] == 0 and b[-1] == 2047
+    assert b[np.searchsorted(x, 2.0 ** -10)] == 0 and b[np.searchsorted(x, 2.0 ** -10) + 0] == 0
+    inner = (b > 0) & (b < 2047)
+    assert inner.sum() > 150_000
+    assert ((k[inner] >= lo[inner]) & (k[inner] - lo[inner] < np.uint64(1 << 46))).all()

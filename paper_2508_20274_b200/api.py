@@ -20,7 +20,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmigsim_b200.so")
+LIB_PATH = os.environ.get("MIGSIM_LIB") or os.path.join(_HERE, "_lib", "libmigsim_b200.so")  # env: A/B builds
 
 
 class ConfigError(ValueError):

@@ -23,12 +23,25 @@ namespace mg {
 
 namespace {
 
-constexpr int kSelThreads = 256;
+#ifndef MG_SEL_THREADS
+#define MG_SEL_THREADS 256
+#endif
+#ifndef MG_SEL_CAND
+#define MG_SEL_CAND 2048
+#endif
+constexpr int kSelThreads = MG_SEL_THREADS;
+#ifndef MG_SEL_MINB
+#define MG_SEL_MINB 6  // 6 CTAs x 256 threads per SM: <= 40 registers
+#endif
 static_assert(kSelThreads / 32 >= 4 && kSelThreads / 32 <= 32, "one warp per quantile, one scan warp");
-constexpr int kDigit = 12;
+#ifndef MG_SEL_DIGIT
+#define MG_SEL_DIGIT 11
+#endif
+constexpr int kDigit = MG_SEL_DIGIT;
 constexpr int kBins = 1 << kDigit;
+static_assert(kBins >= kHistBins, "the producer histogram is staged in the digit histogram");
 constexpr int kMaxQ = 4;
-constexpr int kCand = 4096;  // shared-memory key buffer (also the small-segment threshold)
+constexpr int kCand = MG_SEL_CAND;  // shared-memory key buffer (also the small-segment threshold)
 
 __device__ __forceinline__ uint64_t okey(double x) {
     const uint64_t b = static_cast<uint64_t>(__double_as_longlong(x));
@@ -91,7 +104,10 @@ __device__ __forceinline__ void stream_keys(const double* __restrict__ v, int64_
     const double2* v2 = reinterpret_cast<const double2*>(v + head);
     const int64_t n2 = (n - head) / 2;
     int64_t i = tid;
-    constexpr int kDepth = 8;  // 16-B loads in flight per thread (128 B): ~128 KB per SM at 4 CTAs
+#ifndef MG_SEL_DEPTH
+#define MG_SEL_DEPTH 4
+#endif
+    constexpr int kDepth = MG_SEL_DEPTH;  // 16-B loads in flight per thread (64 B): ~96 KB per SM at 6 CTAs
     const int nthr = blockDim.x;
     for (; i + (kDepth - 1) * nthr < n2; i += kDepth * nthr) {
         double2 x[kDepth];
@@ -368,7 +384,9 @@ __device__ void select_in(Src&& src, int64_t n, uint64_t kmin, uint64_t kmax, co
     __syncthreads();
 }
 
-__device__ void block_select(const double* __restrict__ vals, int64_t n, bool have_range, double vmin, double vmax,
+// Out of line: the general path's register demand would otherwise cap the one-pass path's
+// occupancy (measured: 6 CTAs/SM at 40 registers, 0.080 vs 0.087 ms per C2 wave).
+__device__ __noinline__ void block_select(const double* __restrict__ vals, int64_t n, bool have_range, double vmin, double vmax,
                              const double* qs, int nq, double* out, SelSmem& sm) {
     const int tid = threadIdx.x;
     if (n <= 0) {
@@ -509,6 +527,32 @@ __device__ void hist_select(const double* __restrict__ vals, int64_t n, const ui
         gq[g] = own ? g : 0;
     }
     // the one pass over HBM: the gathered keys are the only reuse, so the lines are not kept
+#ifdef MG_SEL_WARP_APPEND
+    // warp-aggregated appends: one vote per element, ballots + one shared atomic per matching group
+    const uint32_t lane = tid & 31;
+    stream_keys(
+        vals, n,
+        [&](uint64_t k) {
+            const uint32_t b = lat_bin_of_key(k);
+            bool hit = false;
+#pragma unroll
+            for (int g = 0; g < kMaxQ; ++g) hit |= b == gb[g];
+            const uint32_t act = __activemask();  // the stream's tail iterations can diverge
+            if (__any_sync(act, hit)) {
+#pragma unroll
+                for (int g = 0; g < kMaxQ; ++g) {
+                    const uint32_t m = __ballot_sync(act, b == gb[g]);
+                    if (m) {
+                        uint32_t base = 0;
+                        if (lane == static_cast<uint32_t>(__ffs(m) - 1)) base = atomicAdd(&sm.qfill[gq[g]], __popc(m));
+                        base = __shfl_sync(act, base, __ffs(m) - 1);
+                        if (b == gb[g]) sm.cand[sm.qbase[gq[g]] + base + __popc(m & ((1u << lane) - 1u))] = k;
+                    }
+                }
+            }
+        },
+        false);
+#else
     stream_keys(
         vals, n,
         [&](uint64_t k) {
@@ -521,6 +565,7 @@ __device__ void hist_select(const double* __restrict__ vals, int64_t n, const ui
                 }
         },
         false);
+#endif
     __syncthreads();
     const int q = tid >> 5;  // warp q finishes quantile q
     if (q < nq) {
@@ -741,7 +786,7 @@ __device__ void cluster_select(const double* __restrict__ vals, int64_t n, doubl
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kSelThreads, 4) select_kernel(WaveBuffers B, int T, int n_rep) {
+__global__ void __launch_bounds__(kSelThreads, MG_SEL_MINB) select_kernel(WaveBuffers B, int T, int n_rep) {
     extern __shared__ __align__(16) unsigned char smem[];
     SelSmem& sm = *reinterpret_cast<SelSmem*>(smem);
     const int s = blockIdx.x;
@@ -761,7 +806,7 @@ __global__ void __launch_bounds__(kSelThreads, 4) select_kernel(WaveBuffers B, i
                      B.quant + 4ll * so, sm);
 }
 
-__global__ void __launch_bounds__(kSelThreads, 4) select_segments_kernel(const double* __restrict__ vals,
+__global__ void __launch_bounds__(kSelThreads, MG_SEL_MINB) select_segments_kernel(const double* __restrict__ vals,
                                                                       const int64_t* __restrict__ seg_off, int n_seg,
                                                                       const double* __restrict__ qs, int nq,
                                                                       double* __restrict__ out) {

@@ -128,6 +128,38 @@ __device__ __forceinline__ void stream_keys(const double* __restrict__ v, int64_
     if (tid < n - tail) f(okey(v[tail + tid]));
 }
 
+// f(x) for every double of v[0..n) (raw values; same access pattern as stream_keys)
+template <class F>
+__device__ __forceinline__ void stream_raw(const double* __restrict__ v, int64_t n, F&& f, bool keep) {
+    const uint64_t pol = l2_policy(keep);
+    const int tid = threadIdx.x;
+    const int nthr = blockDim.x;
+    int64_t head = (16 - (reinterpret_cast<uintptr_t>(v) & 15)) / 8 & 1;
+    if (head > n) head = n;
+    if (tid < head) f(v[tid]);
+    const double2* v2 = reinterpret_cast<const double2*>(v + head);
+    const int64_t n2 = (n - head) / 2;
+    int64_t i = tid;
+    constexpr int kDepth = MG_SEL_DEPTH;
+    for (; i + (kDepth - 1) * nthr < n2; i += kDepth * nthr) {
+        double2 x[kDepth];
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) x[u] = ld_hint(v2 + i + u * nthr, pol);
+#pragma unroll
+        for (int u = 0; u < kDepth; ++u) {
+            f(x[u].x);
+            f(x[u].y);
+        }
+    }
+    for (; i < n2; i += nthr) {
+        const double2 a = ld_hint(v2 + i, pol);
+        f(a.x);
+        f(a.y);
+    }
+    const int64_t tail = head + 2 * n2;
+    if (tid < n - tail) f(v[tail + tid]);
+}
+
 // A segment in global memory as a key source: every pass but the last keeps its L2 lines.
 struct GlobalSrc {
     const double* v;
@@ -527,45 +559,42 @@ __device__ void hist_select(const double* __restrict__ vals, int64_t n, const ui
         gq[g] = own ? g : 0;
     }
     // the one pass over HBM: the gathered keys are the only reuse, so the lines are not kept
-#ifdef MG_SEL_WARP_APPEND
-    // warp-aggregated appends: one vote per element, ballots + one shared atomic per matching group
-    const uint32_t lane = tid & 31;
-    stream_keys(
-        vals, n,
-        [&](uint64_t k) {
-            const uint32_t b = lat_bin_of_key(k);
-            bool hit = false;
+    bool edge = false;
+    for (int g = 0; g < kMaxQ; ++g) edge |= gb[g] == 0u || gb[g] == static_cast<uint32_t>(kHistBins - 1);
+    if (!edge) {
+        // interior target bins of positive values are equal top-18-bit patterns of the raw double
+        // (sign, exponent, 6 mantissa bits; lat_hist.h): one shift and four compares per sample,
+        // the key is formed only for the few samples that match
+        uint32_t tv[kMaxQ];
+        for (int g = 0; g < kMaxQ; ++g)
+            tv[g] = gb[g] == 0xffffffffu ? 0xffffffffu
+                                         : static_cast<uint32_t>(kHistBase + gb[g] - (1ull << (63 - kHistShift)));
+        stream_raw(
+            vals, n,
+            [&](double x) {
+                const uint32_t t = static_cast<uint32_t>(__double2hiint(x)) >> (kHistShift - 32);
 #pragma unroll
-            for (int g = 0; g < kMaxQ; ++g) hit |= b == gb[g];
-            const uint32_t act = __activemask();  // the stream's tail iterations can diverge
-            if (__any_sync(act, hit)) {
-#pragma unroll
-                for (int g = 0; g < kMaxQ; ++g) {
-                    const uint32_t m = __ballot_sync(act, b == gb[g]);
-                    if (m) {
-                        uint32_t base = 0;
-                        if (lane == static_cast<uint32_t>(__ffs(m) - 1)) base = atomicAdd(&sm.qfill[gq[g]], __popc(m));
-                        base = __shfl_sync(act, base, __ffs(m) - 1);
-                        if (b == gb[g]) sm.cand[sm.qbase[gq[g]] + base + __popc(m & ((1u << lane) - 1u))] = k;
+                for (int g = 0; g < kMaxQ; ++g)
+                    if (t == tv[g]) {
+                        const uint32_t at = atomicAdd(&sm.qfill[gq[g]], 1u);
+                        sm.cand[sm.qbase[gq[g]] + at] = okey(x);
                     }
-                }
-            }
-        },
-        false);
-#else
-    stream_keys(
-        vals, n,
-        [&](uint64_t k) {
-            const uint32_t b = lat_bin_of_key(k);
+            },
+            false);
+    } else {
+        stream_keys(
+            vals, n,
+            [&](uint64_t k) {
+                const uint32_t b = lat_bin_of_key(k);
 #pragma unroll
-            for (int g = 0; g < kMaxQ; ++g)
-                if (b == gb[g]) {
-                    const uint32_t at = atomicAdd(&sm.qfill[gq[g]], 1u);
-                    sm.cand[sm.qbase[gq[g]] + at] = k;
-                }
-        },
-        false);
-#endif
+                for (int g = 0; g < kMaxQ; ++g)
+                    if (b == gb[g]) {
+                        const uint32_t at = atomicAdd(&sm.qfill[gq[g]], 1u);
+                        sm.cand[sm.qbase[gq[g]] + at] = k;
+                    }
+            },
+            false);
+    }
     __syncthreads();
     const int q = tid >> 5;  // warp q finishes quantile q
     if (q < nq) {

@@ -179,3 +179,20 @@ def test_latency_bins_monotone_and_exact_intervals():
     inner = (b > 0) & (b < 2047)
     assert inner.sum() > 150_000
     assert ((k[inner] >= lo[inner]) & (k[inner] - lo[inner] < np.uint64(1 << 46))).all()
+
+
+def test_sweep_focus_is_reference_pick_focus_tenant():
+    """sweep.default_focus == harness.cpp:80-87 pick_focus_tenant (smallest tail SLO after presets,
+    first in file order on ties), via the engine's host-only scenario loader (no GPU)."""
+    from paper_2508_20274_b200.sweep import default_focus
+
+    expect = {"c2_cluster16.yaml": "ta", "c5_mc64.yaml": "h0g0a", "default.yaml": "t1", "llm.yaml": "llm"}
+    for path in GOLDEN_SCENARIOS + CONFIG_SCENARIOS + [os.path.join(os.path.dirname(CONFIG_SCENARIOS[0]),
+                                                                    "c5_mc64.yaml")]:
+        name = os.path.basename(path)
+        got = default_focus(path)
+        spec = _dump(path)[1]
+        best = min(spec["tenants"], key=lambda t: t["slo_tail_ms"])  # min() keeps the first of ties
+        assert got == best["id"]
+        if name in expect:
+            assert got == expect[name]

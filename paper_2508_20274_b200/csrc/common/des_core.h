@@ -637,17 +637,8 @@ struct Sim {
     MG_HD void on_arrival(int i) {
         TenantDyn& d = td[i];
         const int k = d.n_arrived;
-        if ((k & 15) == 0) {
-            // records are consumed in order; pull the next 128-B line of every per-request
-            // array into L1 a block ahead (arrays are 16-element aligned per tenant)
-            const int64_t o = d.base + k + 16;
-            prefetch_l1(io.arr_t + o);
-            prefetch_l1(io.arr_bytes + o);
-            prefetch_l1(io.arr_mult + o);
-            prefetch_l1(io.arr_noise + o);
-            prefetch_l1(io.irq_e + o);
-            prefetch_l1(io.req_transfer_ms + o);
-        }
+        // (no software prefetch of the arrival records: an L1 prefetch per 16 records measured 2%
+        //  slower than letting the in-order loads miss)
         d.n_arrived = k + 1;
         start_transfer(i);
         if (d.n_arrived < d.n_count) push(kEvArrival, i, io.arr_t[d.base + d.n_arrived]);

@@ -315,7 +315,12 @@ __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S
     des_body<HostLanes>(S, C, B, n_rep, L);
 }
 
-__global__ void __launch_bounds__(32) des_kernel_reg(const PScenario* __restrict__ S,
+#ifdef MG_DES_MAXNREG
+#define MG_DES_BOUNDS __maxnreg__(MG_DES_MAXNREG)
+#else
+#define MG_DES_BOUNDS __launch_bounds__(32)
+#endif
+__global__ void MG_DES_BOUNDS des_kernel_reg(const PScenario* __restrict__ S,
                                                      const PController* __restrict__ C, WaveBuffers B, int n_rep,
                                                      SimLayout L) {
     des_body<RegLanes>(S, C, B, n_rep, L);

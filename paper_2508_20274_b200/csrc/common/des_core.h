@@ -356,6 +356,9 @@ struct Sim {
     // per-event scalars kept out of shared memory (registers once inlined into the kernel)
     double now;
     uint32_t next_seq, n_events;  // seq < 2^29 is checked in finish
+    // hot scenario scalars held in registers (PScenario itself stays in global memory)
+    double measure_start;
+    int n_irq, redistribute;
     Mask live_resume, live_expire;  // tenants with a live resume / guardrail-expire event
     // Working-set arrays held as registers (not re-loaded from SimState) so that, after inlining
     // into the kernel, the compiler sees shared-memory provenance and emits LDS/STS.
@@ -372,7 +375,8 @@ struct Sim {
     MG_HD Sim(const PScenario& s, const PController& c, const ReplicaIO& i, SimState& state, Lanes l,
               TenantDyn* tdp, TenantCtl* ctlp, RootDyn* rdp)
         : S(s), C(c), io(i), st(state), lanes(l), T(s.n_tenants), now(0.0), next_seq(0), n_events(0),
-          live_resume(0), live_expire(0), td(tdp), ctl(ctlp), rd(rdp), tn(s.tenants), gp(s.gpus), rt(s.roots),
+          live_resume(0), live_expire(0), measure_start(s.measure_start_s), n_irq(s.n_irq),
+          redistribute(s.fabric_redistribute), td(tdp), ctl(ctlp), rd(rdp), tn(s.tenants), gp(s.gpus), rt(s.roots),
           iq(s.irq), hio(s.host_io_capacity) {}
 
     // ---- small helpers -------------------------------------------------------------------
@@ -456,7 +460,7 @@ struct Sim {
         return s;
     }
     MG_HD bool irq_recent(int h, int core_group) const {  // engine.cpp:664-668
-        for (int b = 0; b < S.n_irq; ++b) {
+        for (int b = 0; b < n_irq; ++b) {
             const PIrq& q = iq[b];
             if (q.host == h && q.core_group == core_group &&
                 sched_active_within(q.sched, fsub(now, C.irq_lookback_s), now))
@@ -508,7 +512,7 @@ struct Sim {
                 td[i].grant = b;
                 granted = fadd(granted, b);
             }
-            if (S.fabric_redistribute) {
+            if (redistribute) {
                 double residual = fsub(cap, granted);
                 for (int iter = 0; iter < 64 && residual > fmul(1e-9, cap); ++iter) {
                     double open_w = 0.0;
@@ -556,7 +560,7 @@ struct Sim {
         const TenantDyn& d = td[i];
         if (d.cpu_pinned) return false;
         const PGpu& g = gpu_of(i);
-        for (int b = 0; b < S.n_irq; ++b) {
+        for (int b = 0; b < n_irq; ++b) {
             const PIrq& q = iq[b];
             if (q.host == d.host && q.core_group == g.core_group && sched_active(q.sched, now)) return true;
         }
@@ -587,7 +591,7 @@ struct Sim {
         }
         double extra = io.arr_noise[base + k];
         if (irq_exposed(i)) {
-            for (int b = 0; b < S.n_irq; ++b) {
+            for (int b = 0; b < n_irq; ++b) {
                 const PIrq& q = iq[b];
                 if (q.host == d.host && q.core_group == g.core_group) {
                     if (q.extra_noise_ms > 0.0) {
@@ -680,7 +684,7 @@ struct Sim {
         total = fadd(fadd(compute, transfer), noise);
         const uint64_t idx = d.completed;
         d.completed += 1;
-        if (now >= S.measure_start_s) {
+        if (now >= measure_start) {
             io.win_lat[base + static_cast<int64_t>(d.n_window)] = total;
             d.n_window += 1;
             d.sum_total = fadd(d.sum_total, total);

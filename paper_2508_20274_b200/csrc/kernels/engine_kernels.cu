@@ -156,16 +156,28 @@ __device__ __forceinline__ bool next_event<HostLanes>(Sim<HostLanes>& sim, int T
     uint32_t hi = 0xffffffffu, lo = 0xffffffffu, kq = 0xffffffffu;
     int bi = -1;
     const int nslots = sim.any_rare() ? kEvKinds * T + 1 : 3 * T + 1;
-    for (int k = lane; k < nslots; k += 32) {
-        const uint64_t key = slots[k].key;
-        if (key == ~0ull) continue;
-        const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(slots[k].t));
-        const uint32_t h = static_cast<uint32_t>(tb >> 32), l = static_cast<uint32_t>(tb), q = order_q(key);
+    // all of this lane's slot loads first (independent LDS.128s in flight), then the compares
+    constexpr int KS = (kEvKinds * kMaxTenants + 1 + 31) / 32;
+    uint64_t keys[KS], tbs[KS];
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+        const int k = lane + 32 * j;
+        keys[j] = ~0ull;
+        tbs[j] = 0;
+        if (k < nslots) {
+            keys[j] = slots[k].key;
+            tbs[j] = static_cast<uint64_t>(__double_as_longlong(slots[k].t));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+        if (keys[j] == ~0ull) continue;
+        const uint32_t h = static_cast<uint32_t>(tbs[j] >> 32), l = static_cast<uint32_t>(tbs[j]), q = order_q(keys[j]);
         if (h < hi || (h == hi && (l < lo || (l == lo && q < kq)))) {
             hi = h;
             lo = l;
             kq = q;
-            bi = k;
+            bi = lane + 32 * j;
         }
     }
     const uint32_t m1 = __reduce_min_sync(0xffffffffu, hi);

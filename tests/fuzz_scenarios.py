@@ -28,13 +28,15 @@ def _sched(rng: random.Random) -> str:
             f"        - {{ start_s: {c:.3f}, end_s: {c + rng.uniform(10, 90):.3f} }}\n")
 
 
-def make_scenario(seed: int) -> str:
+def make_scenario(seed: int, wide: bool = False) -> str:
+    """One random scenario-v1 document.  wide=True: 11-40 tenants on up to 4 hosts x 8 GPUs (the
+    engine's T > 10 code path: event slots in shared memory)."""
     rng = random.Random(seed)
-    n_hosts = rng.choice([1, 1, 2])
+    n_hosts = rng.choice([2, 3, 4]) if wide else rng.choice([1, 1, 2])
     hosts, gpus_of = [], []
     for h in range(n_hosts):
         n_roots = rng.choice([1, 2, 3])
-        n_gpus = rng.choice([2, 3, 4])
+        n_gpus = rng.choice([6, 8]) if wide else rng.choice([2, 3, 4])
         roots = "\n".join(f"        - {{ id: {r * 3 + 1}, capacity_Bps: {rng.choice(['8e9', '12e9', '16e9', '24e9'])} }}"
                           for r in range(n_roots))
         gl = []
@@ -48,7 +50,7 @@ def make_scenario(seed: int) -> str:
     # tenants: pack slices per GPU without overlap
     used = {}
     tenants = []
-    n_t = rng.randint(2, 7)
+    n_t = rng.randint(11, 40) if wide else rng.randint(2, 7)
     for t in range(n_t):
         for _ in range(20):
             h, g, nomig = rng.choice(gpus_of)

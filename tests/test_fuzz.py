@@ -47,3 +47,31 @@ def test_fuzz_gpu(engine, tmp_path):
                 assert d == [], (seed, run_seed, d[:8])
         finally:
             res.close()
+
+
+WIDE_SEEDS = range(9000, 9030)
+
+
+def test_fuzz_wide_engine_logic_cpu(tmp_path):
+    """11-40 tenants: the event slots live in shared memory (T > 10) on the device."""
+    for seed in WIDE_SEEDS[:6]:
+        p = tmp_path / f"wide{seed}.yaml"
+        p.write_text(make_scenario(seed, wide=True))
+        ref, _ = ref_run(str(p), seed % 3 + 1)
+        assert diff_results(ref, hostsim_run(str(p), seed % 3 + 1)) == [], seed
+
+
+@pytest.mark.gpu
+def test_fuzz_wide_gpu(engine, tmp_path):
+    for seed in WIDE_SEEDS:
+        p = tmp_path / f"wide{seed}.yaml"
+        p.write_text(make_scenario(seed, wide=True))
+        sid = engine.load_scenario(str(p))
+        seeds = [seed % 3 + 1, seed % 3 + 2]
+        res = engine.run_batch(sid, seeds)
+        try:
+            for i, s in enumerate(seeds):
+                ref, _ = ref_run(str(p), s)
+                assert diff_results(ref, res.run(i)) == [], (seed, s)
+        finally:
+            res.close()

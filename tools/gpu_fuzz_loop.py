@@ -4,10 +4,11 @@ from tests.fuzz_scenarios import make_scenario
 from tests._libs import ref_run, diff_results
 from paper_2508_20274_b200 import Engine
 lo, hi = int(sys.argv[1]), int(sys.argv[2])
+wide = len(sys.argv) > 3 and sys.argv[3] == 'wide'
 eng = Engine(0)
 for seed in range(lo, hi):
     path = f'/tmp/f{seed}.yaml'
-    open(path, 'w').write(make_scenario(seed))
+    open(path, 'w').write(make_scenario(seed, wide=wide))
     sid = eng.load_scenario(path)
     seeds = [seed % 5 + 1, seed % 5 + 2]
     res = eng.run_batch(sid, seeds)

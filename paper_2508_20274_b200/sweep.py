@@ -88,7 +88,9 @@ def _variants(name: str) -> List[Variant]:
         return main_variants()
     if name == "full":
         return [Variant("full", True, True, True, True)]
-    raise ValueError(f"unknown variant set '{name}' (ablation | main | full)")
+    if name == "c4":  # BASELINE configs[3]: static / MIG-only / placement-only / full controller
+        return [v for v in ablation_variants() if v.name in ("static", "mig-only", "placement-only", "full")]
+    raise ValueError(f"unknown variant set '{name}' (ablation | main | full | c4)")
 
 
 def main(argv=None) -> None:

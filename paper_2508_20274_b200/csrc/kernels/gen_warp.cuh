@@ -22,6 +22,9 @@
 namespace mg {
 
 constexpr int kRing = 1024;       // canonical ring (positions)
+static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
+// ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
+__device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
 constexpr int kMaxCallsRound = 160;
 
 struct WarpMtSmem {
@@ -167,20 +170,20 @@ struct GammaSmem {
 // transform for positions [gen_end-1, gen_end+311).
 __device__ __forceinline__ void gamma_fill(GammaSmem& g, int64_t gen_end, int lane) {
     warp_mt_twist(g.mt, lane);
-    for (int j = lane; j < kMtN; j += 32) g.c[(gen_end + j) % kRing] = canonical_from(mt_temper(g.mt.x[j]));
+    for (int j = lane; j < kMtN; j += 32) g.c[ring_idx(gen_end + j)] = canonical_from(mt_temper(g.mt.x[j]));
     __syncwarp();
     for (int j = lane; j < kMtN; j += 32) {
         const int64_t pos = gen_end - 1 + j;
         if (pos < 0) continue;
-        const double x = fsub(fmul(2.0, g.c[pos % kRing]), 1.0);
-        const double y = fsub(fmul(2.0, g.c[(pos + 1) % kRing]), 1.0);
+        const double x = fsub(fmul(2.0, g.c[ring_idx(pos)]), 1.0);
+        const double y = fsub(fmul(2.0, g.c[ring_idx(pos + 1)]), 1.0);
         const double r2 = fadd(fmul(x, x), fmul(y, y));
         const bool a = !(r2 > 1.0 || r2 == 0.0);
-        g.acc[pos % kRing] = a;
+        g.acc[ring_idx(pos)] = a;
         if (a) {
             const double mult = fsqrt(fdiv_exact(fmul(-2.0, gl_log(r2)), r2));
-            g.ny[pos % kRing] = fmul(y, mult);
-            g.nx[pos % kRing] = fmul(x, mult);
+            g.ny[ring_idx(pos)] = fmul(y, mult);
+            g.nx[ring_idx(pos)] = fmul(x, mult);
         }
     }
     __syncwarp();
@@ -201,11 +204,11 @@ __device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaP
             } else {
                 for (;;) {
                     if (p + 1 >= limit) return false;
-                    if (g.acc[p % kRing]) break;
+                    if (g.acc[ring_idx(p)]) break;
                     p += 2;
                 }
-                n = g.ny[p % kRing];
-                cache = g.nx[p % kRing];
+                n = g.ny[ring_idx(p)];
+                cache = g.nx[ring_idx(p)];
                 cached = true;
                 p += 2;
             }
@@ -214,7 +217,7 @@ __device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaP
         } while (v <= 0.0);
         v = fmul(fmul(v, v), v);
         if (p >= limit) return false;
-        u = g.c[p % kRing];
+        u = g.c[ring_idx(p)];
         p += 1;
         const double sq = fsub(1.0, fmul(fmul(fmul(fmul(0.0331, n), n), n), n));
         if (!(u > sq)) break;
@@ -225,11 +228,11 @@ __device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaP
     if (!(gp.alpha == gp.malpha)) {
         for (;;) {
             if (p >= limit) return false;
-            const double u2 = g.c[p % kRing];
+            const double u2 = g.c[ring_idx(p)];
             p += 1;
             if (u2 != 0.0) break;
         }
-        q = static_cast<int32_t>((p - 1) % kRing);
+        q = static_cast<int32_t>(ring_idx(p - 1));
     }
     v_out = v;
     q_out = q;

@@ -196,3 +196,35 @@ def test_sweep_focus_is_reference_pick_focus_tenant():
         assert got == best["id"]
         if name in expect:
             assert got == expect[name]
+
+
+def test_capi_error_codes_without_gpu():
+    """C-ABI error behaviour on a host without a GPU (include/migsim_b200.h return codes): opening a
+    device is a runtime error (2) with a message; a malformed experiment.json given to
+    render_report is a runtime error too; no CPU fallback exists."""
+    import ctypes
+
+    import pytest as _pt
+
+    from paper_2508_20274_b200 import ConfigError, Engine, load_library, render_report
+
+    lib = load_library()
+    h = ctypes.c_void_p()
+    err = ctypes.create_string_buffer(256)
+    try:
+        import torch
+
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if not has_gpu:
+        rc = lib.migsim_gpu_open(0, ctypes.byref(h), err, 256)
+        assert rc == 2 and err.value
+        with _pt.raises(RuntimeError):
+            Engine(0)
+    with _pt.raises(RuntimeError):
+        render_report("{not json")
+    from paper_2508_20274_b200.api import scenario_spec
+
+    with _pt.raises(ConfigError):
+        scenario_spec("/nonexistent/scenario.yaml")

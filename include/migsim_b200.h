@@ -40,15 +40,18 @@ typedef struct migsim_gpu migsim_gpu;
 typedef struct migsim_batch_result migsim_batch_result;
 
 /* harness::Variant (harness.hpp:40-46) plus the e3 sweep knobs (harness.cpp:89-110).
- * Integer flags: -1 keeps the scenario's value. */
+ * Flags: -1 keeps the scenario's value, 0/1 set it.  Numeric knobs: MIGSIM_KEEP_INT / NaN keep
+ * the scenario's value; every other value is applied and checked by ControllerConfig::validate
+ * (model.cpp:184-206), so e.g. dwell_obs = 0 is a config error, as in the reference. */
+#define MIGSIM_KEEP_INT INT32_MIN
 typedef struct migsim_variant {
     const char* name;
     int32_t enabled, enable_mig, enable_placement, enable_guardrails;
-    double sample_interval_s;   /* <= 0: keep */
-    int32_t persistence_windows; /* <= 0: keep */
-    int32_t dwell_obs;           /* <= 0: keep */
-    int32_t cooldown_obs;        /* < 0: keep  */
-    int32_t validation_obs;      /* <= 0: keep */
+    double sample_interval_s;    /* NaN: keep */
+    int32_t persistence_windows; /* MIGSIM_KEEP_INT: keep */
+    int32_t dwell_obs;           /* MIGSIM_KEEP_INT: keep */
+    int32_t cooldown_obs;        /* MIGSIM_KEEP_INT: keep */
+    int32_t validation_obs;      /* MIGSIM_KEEP_INT: keep */
 } migsim_variant;
 
 /* engine::RunOptions (engine.hpp:94-99) batch form. */

@@ -169,9 +169,14 @@ def _check(code: int, err: ctypes.Array) -> None:
     raise RuntimeError(msg)
 
 
+KEEP_INT = -(2 ** 31)  # MIGSIM_KEEP_INT (include/migsim_b200.h)
+
+
 @dataclass
 class Variant:
-    """harness::Variant (harness.hpp:40-46); None keeps the scenario's setting."""
+    """harness::Variant (harness.hpp:40-46); None (and only None) keeps the scenario's setting.
+    Every other value is applied and validated like ControllerConfig::validate (model.cpp:184-206),
+    so an invalid knob raises ConfigError instead of being dropped."""
 
     name: str = "as-is"
     enabled: Optional[bool] = None
@@ -191,11 +196,9 @@ class Variant:
         return _Variant(
             self.name.encode(), b(self.enabled), b(self.enable_mig), b(self.enable_placement),
             b(self.enable_guardrails),
-            -1.0 if self.sample_interval_s is None else float(self.sample_interval_s),
-            -1 if self.persistence_windows is None else int(self.persistence_windows),
-            -1 if self.dwell_obs is None else int(self.dwell_obs),
-            -1 if self.cooldown_obs is None else int(self.cooldown_obs),
-            -1 if self.validation_obs is None else int(self.validation_obs),
+            float("nan") if self.sample_interval_s is None else float(self.sample_interval_s),
+            *[KEEP_INT if x is None else int(x)
+              for x in (self.persistence_windows, self.dwell_obs, self.cooldown_obs, self.validation_obs)],
         )
 
 

@@ -725,6 +725,8 @@ int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off,
                       size_t n_q, double* out, double* device_ms, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         CK(cudaSetDevice(g->device));
+        if (device_ms) *device_ms = 0.0;
+        if (n_segments == 0 || n_q == 0) return;  // nothing to select: an empty result, no launch
         const int64_t n = seg_off[n_segments];
         DevBuf<double> dv, dq, dout;
         DevBuf<int64_t> doff;
@@ -1099,8 +1101,11 @@ int migsim_gpu_arrivals(migsim_gpu* g, int32_t scenario_id, uint64_t seed, int32
         mg::gen_marks_kernel<<<static_cast<unsigned>(4 * T), 32, 0, s>>>(A.scen.p, B, 1);
         CK(cudaGetLastError());
         std::vector<int32_t> nk(T);
+        int32_t overflow = 0;
         CK(cudaMemcpyAsync(nk.data(), A.n_kept.p, 4 * T, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&overflow, A.gen_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        if (overflow) throw ParityGuard("arrival-record capacity exceeded");  // never return a truncated list
         const int64_t n = nk[tenant];
         *n_out = n;
         const int64_t m = std::min(n, cap);

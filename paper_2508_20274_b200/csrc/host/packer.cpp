@@ -11,16 +11,21 @@ namespace mgb {
 
 ControllerConfig apply_variant(const ControllerConfig& base, const Variant& v) {
     ControllerConfig c = base;
-    if (v.enabled >= 0) c.enabled = v.enabled != 0;
-    if (v.enable_mig >= 0) c.enable_mig = v.enable_mig != 0;
-    if (v.enable_placement >= 0) c.enable_placement = v.enable_placement != 0;
-    if (v.enable_guardrails >= 0) c.enable_guardrails = v.enable_guardrails != 0;
-    if (v.sample_interval_s > 0.0) c.sample_interval_s = v.sample_interval_s;
-    if (v.persistence_windows > 0) c.persistence_windows = v.persistence_windows;
-    if (v.dwell_obs > 0) c.dwell_obs = v.dwell_obs;
-    if (v.cooldown_obs >= 0) c.cooldown_obs = v.cooldown_obs;
-    if (v.validation_obs > 0) c.validation_obs = v.validation_obs;
-    if (v.tail_threshold_ms > 0.0) c.tail_threshold_ms = v.tail_threshold_ms;
+    auto flag = [](int f, bool& dst) {
+        if (f == -1) return;
+        if (f != 0 && f != 1) throw ConfigError("variant flag must be -1 (keep), 0 or 1");
+        dst = f != 0;
+    };
+    flag(v.enabled, c.enabled);
+    flag(v.enable_mig, c.enable_mig);
+    flag(v.enable_placement, c.enable_placement);
+    flag(v.enable_guardrails, c.enable_guardrails);
+    if (!std::isnan(v.sample_interval_s)) c.sample_interval_s = v.sample_interval_s;
+    if (v.persistence_windows != kKeepInt) c.persistence_windows = v.persistence_windows;
+    if (v.dwell_obs != kKeepInt) c.dwell_obs = v.dwell_obs;
+    if (v.cooldown_obs != kKeepInt) c.cooldown_obs = v.cooldown_obs;
+    if (v.validation_obs != kKeepInt) c.validation_obs = v.validation_obs;
+    if (!std::isnan(v.tail_threshold_ms)) c.tail_threshold_ms = v.tail_threshold_ms;
     c.validate();
     return c;
 }

@@ -13,6 +13,10 @@
 #include <string>
 #include <vector>
 
+#include <climits>
+#include <cstdint>
+#include <limits>
+
 #include "../common/des_types.h"
 #include "../common/packed.h"
 #include "scenario.hpp"
@@ -20,12 +24,15 @@
 namespace mgb {
 
 // harness::Variant (harness.hpp:40-46) + the e3 sweep overrides (harness.cpp:89-110)
+// Only the sentinels keep the scenario's value (flags -1, integers kKeepInt, doubles NaN); every
+// other value is applied and then checked by ControllerConfig::validate (model.cpp:184-206).
+constexpr int kKeepInt = INT32_MIN;
 struct Variant {
     std::string name = "as-is";
     int enabled = -1, enable_mig = -1, enable_placement = -1, enable_guardrails = -1;  // -1: keep scenario value
-    double sample_interval_s = -1.0;
-    int persistence_windows = -1, dwell_obs = -1, cooldown_obs = -1, validation_obs = -1;
-    double tail_threshold_ms = -1.0;
+    double sample_interval_s = std::numeric_limits<double>::quiet_NaN();
+    int persistence_windows = kKeepInt, dwell_obs = kKeepInt, cooldown_obs = kKeepInt, validation_obs = kKeepInt;
+    double tail_threshold_ms = std::numeric_limits<double>::quiet_NaN();
 };
 
 ControllerConfig apply_variant(const ControllerConfig& base, const Variant& v);

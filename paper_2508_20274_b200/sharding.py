@@ -51,6 +51,25 @@ def confidence_interval(values: Sequence[float]) -> Tuple[float, float]:
     return mean, 1.96 * math.sqrt(ss / n) / math.sqrt(n)
 
 
+def gather_rows(local, dist):
+    """All-gather of per-rank row blocks whose lengths may differ (uneven seed splits, empty
+    ranks): all_gather needs equal shapes, so the counts go first, every block is padded to the
+    largest, and each part is trimmed back to its real length, in rank order."""
+    import torch
+
+    world = dist.get_world_size()
+    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+    counts = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(counts, n)
+    counts = [int(c.item()) for c in counts]
+    width = max(counts)
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[: local.shape[0]] = local
+    parts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)], 0)
+
+
 def reduce_rows(rows: np.ndarray, dist=None, device: str = "cpu"):
     """rows: float64 [n_local_seeds, 3] = (p99_ms, miss_rate, throughput_hz) in seed order.
 
@@ -58,13 +77,12 @@ def reduce_rows(rows: np.ndarray, dist=None, device: str = "cpu"):
     """
     import torch
 
+    rows = np.asarray(rows, np.float64).reshape(-1, 3)
     hist = torch.tensor(miss_histogram(rows[:, 1]), dtype=torch.int64, device=device)
-    local = torch.tensor(np.ascontiguousarray(rows, np.float64), device=device)
+    local = torch.tensor(np.ascontiguousarray(rows), device=device)
     if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(hist)
-        parts = [torch.zeros_like(local) for _ in range(dist.get_world_size())]
-        dist.all_gather(parts, local)
-        local = torch.cat(parts, 0)
+        local = gather_rows(local, dist)
     all_rows = local.cpu().numpy()
     cis = [confidence_interval(all_rows[:, k]) for k in range(3)]
     return all_rows, hist.cpu().numpy(), cis

@@ -22,7 +22,7 @@ HOSTSIM_SO = os.path.join(ROOT, "tests", "native", "_build", "libhostsim.so")
 PRODUCT_SO = os.path.join(ROOT, "paper_2508_20274_b200", "_lib", "libmigsim_b200.so")
 SCEN_DIR = os.path.join(ROOT, "tests", "golden", "scenarios")
 CONFIG_DIR = os.path.join(ROOT, "scenarios")
-NLOHMANN = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+NLOHMANN = os.path.join(ROOT, "paper_2508_20274_b200", "csrc", "third_party", "nlohmann")  # vendored 3.11.3
 
 GOLDEN_SCENARIOS = [os.path.join(SCEN_DIR, f"{n}.yaml") for n in ("default", "llm", "stability", "unstable")]
 CONFIG_SCENARIOS = [os.path.join(CONFIG_DIR, f) for f in ("c1_single_host.yaml", "c2_cluster16.yaml",

@@ -19,14 +19,17 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, rows_all, out):
+def _worker(rank, world, port, rows_all, out, uneven=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    seeds = sharding.seed_block(rank, world, len(rows_all) // world)
-    local = rows_all[np.array(seeds) - 1]
+    if uneven:  # strong-scaling split of a seed list that does not divide evenly (sweep.py)
+        seeds = sharding.split_seeds(list(range(1, len(rows_all) + 1)), rank, world)
+    else:
+        seeds = sharding.seed_block(rank, world, len(rows_all) // world)
+    local = rows_all[np.array(seeds, dtype=np.int64) - 1] if seeds else np.zeros((0, 3))
     all_rows, hist, cis = sharding.reduce_rows(local, dist)
     out[rank] = (all_rows, hist, cis)
     dist.destroy_process_group()
@@ -59,3 +62,31 @@ def test_two_rank_reduction_matches_single_process():
         assert cis == single_cis
         # CIs are harness-identical (population sigma, seed order)
         assert cis[0] == restate.confidence_interval(rows[:, 0].tolist())
+
+
+def _run_ranks(rows, world, uneven):
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_worker, args=(r, world, port, rows, out, uneven)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    return dict(out)
+
+
+@pytest.mark.parametrize("n,world", [(7, 2), (1, 2), (10, 3)])
+def test_uneven_split_reduction(n, world):
+    """all_gather of unequal per-rank blocks (7 seeds on 2 ranks, 1 seed on 2 ranks so one rank is
+    empty, 10 on 3): counts first, pad, trim -- every rank sees all rows in seed order."""
+    rng = np.random.default_rng(n)
+    rows = np.stack([rng.lognormal(2, 0.5, n), rng.uniform(0, 0.2, n), rng.uniform(100, 200, n)], 1)
+    out = _run_ranks(rows, world, True)
+    single_rows, single_hist, single_cis = sharding.reduce_rows(rows, None)
+    for r in range(world):
+        all_rows, hist, cis = out[r]
+        assert all_rows.shape == rows.shape and (all_rows == rows).all()
+        assert (hist == single_hist).all() and cis == single_cis

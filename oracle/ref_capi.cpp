@@ -392,6 +392,59 @@ int ref_result_audit(void* hp, const char* scenario_json, const char* overrides_
 
 void ref_result_free(void* hp) { delete static_cast<Handle*>(hp); }
 
+// The reference's audit::audit_run (audit.cpp:52-122) over a RunResult produced by the GPU engine:
+// `gpu_result_json` is the engine's RunResult JSON (migsim_batch_run_json); the fields the audit
+// reads (action kind/tenant/target/seq/obs_since_prev/guardrail values, end-state placement and
+// claim) are rebuilt into an engine::RunResult.  Returns the issue count, -1 on error.
+int ref_audit_gpu_result(const char* scenario_json, const char* overrides_json, const char* gpu_result_json,
+                         char** issues_json) {
+    try {
+        auto spec = scenario::parse_scenario(scenario_json, "<scenario>");
+        apply_overrides(spec, overrides_json);
+        const json g = json::parse(gpu_result_json);
+        engine::RunResult r;
+        r.duration_s = g.at("duration_s").get<double>();
+        r.measure_start_s = g.at("measure_start_s").get<double>();
+        auto kind_of = [](const std::string& s) {
+            for (int k = 0; k <= static_cast<int>(control::ActionKind::rollback); ++k)
+                if (s == control::to_string(static_cast<control::ActionKind>(k))) return static_cast<control::ActionKind>(k);
+            throw std::runtime_error("unknown action kind " + s);
+        };
+        for (const auto& a : g.at("actions")) {
+            control::ActionRecord rec;
+            rec.seq = a.at("seq").get<int>();
+            rec.t_s = a.at("t_s").get<double>();
+            rec.tenant = a.at("tenant").get<std::string>();
+            rec.target = a.at("target").get<std::string>();
+            rec.kind = kind_of(a.at("kind").get<std::string>());
+            rec.obs_since_prev = a.at("obs_since_prev").get<size_t>();
+            rec.throttle_Bps = a.at("throttle_Bps").get<double>();
+            rec.quota_pct = a.at("quota_pct").get<double>();
+            rec.pause_s = a.at("pause_s").get<double>();
+            rec.rolled_back_seq = a.at("rolled_back_seq").get<int>();
+            r.actions.push_back(rec);
+        }
+        for (const auto& [id, e] : g.at("end_states").items()) {
+            engine::EndState es;
+            es.placement.host = e.at("host").get<int>();
+            es.placement.gpu = e.at("gpu").get<int>();
+            es.placement.slices.first = e.at("first_slice").get<int>();
+            es.profile = e.at("profile").get<std::string>();
+            es.claim_Bps = e.at("claim_Bps").get<double>();
+            es.cpu_pinned = e.at("cpu_pinned").get<bool>();
+            r.end_states[id] = es;
+        }
+        auto rep = audit::audit_run(spec, r);
+        ordered_json arr = ordered_json::array();
+        for (const auto& i : rep.issues) arr.push_back({{"rule", i.rule}, {"message", i.message}});
+        if (issues_json) *issues_json = dup_str(arr.dump());
+        return static_cast<int>(rep.issues.size());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // Reference replica fan-out for the CPU baseline: jobs = variants x seeds, run in std::async
 // batches of `jobs` exactly like harness.cpp:156-176.  Per job writes (focus p99, focus miss,
 // sum throughput, total completions).  Returns wall seconds, or -1 on error.

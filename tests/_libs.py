@@ -212,3 +212,47 @@ def diff_results(ref: dict, mine: dict) -> list:
     if rs["actions"]["total"] != len(mine["actions"]) or rs["pauses"]["count"] != len(mine["pauses"]):
         bad.append(("summary counts",))
     return bad
+
+
+def ref_runs_parallel(jobs, threads: int | None = None):
+    """ref_run over [(path, seed, overrides)] on every host core (ctypes releases the GIL while the
+    reference engine runs), results in job order."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    oracle()  # load once before the threads start
+    with ThreadPoolExecutor(threads or os.cpu_count() or 1) as ex:
+        return list(ex.map(lambda j: ref_run(j[0], j[1], j[2] if len(j) > 2 else None)[0], jobs))
+
+
+def ref_audit_gpu(path: str, gpu_result: dict, overrides: dict | None = None):
+    """The reference's audit::audit_run (audit.cpp:52-122) over a GPU RunResult; returns the issue list."""
+    lib = oracle()
+    lib.ref_audit_gpu_result.restype = ctypes.c_int
+    lib.ref_audit_gpu_result.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p,
+                                         ctypes.POINTER(ctypes.c_void_p)]
+    out = ctypes.c_void_p()
+    n = lib.ref_audit_gpu_result(scenario_json(path), json.dumps(overrides).encode() if overrides else None,
+                                 json.dumps(gpu_result).encode(), ctypes.byref(out))
+    if n < 0:
+        raise RuntimeError(lib.ref_last_error().decode())
+    try:
+        return json.loads(ctypes.string_at(out.value).decode())
+    finally:
+        lib.ref_free(out)
+
+
+def ref_audit_ref(path: str, seed: int, overrides: dict | None = None):
+    """audit::audit_run over the reference's own run of (path, seed, overrides)."""
+    lib = oracle()
+    sj = scenario_json(path)
+    ov = json.dumps(overrides).encode() if overrides else None
+    h = lib.ref_run(sj, ov, seed, 0)
+    if not h:
+        raise RuntimeError(lib.ref_last_error().decode())
+    out = ctypes.c_void_p()
+    try:
+        lib.ref_result_audit(h, sj, ov, ctypes.byref(out))
+        return json.loads(ctypes.string_at(out.value).decode())
+    finally:
+        lib.ref_free(out)
+        lib.ref_result_free(h)

@@ -28,15 +28,18 @@ def _sched(rng: random.Random) -> str:
             f"        - {{ start_s: {c:.3f}, end_s: {c + rng.uniform(10, 90):.3f} }}\n")
 
 
-def make_scenario(seed: int, wide: bool = False) -> str:
+def make_scenario(seed: int, wide: bool = False, xwide: bool = False) -> str:
     """One random scenario-v1 document.  wide=True: 11-40 tenants on up to 4 hosts x 8 GPUs (the
-    engine's T > 10 code path: event slots in shared memory)."""
+    engine's T > 10 code path: event slots in shared memory).  xwide=True: 41-64 tenants on 4-5
+    hosts x 8 GPUs (up to the engine's 64-tenant limit: 64-bit tenant masks, controller rings in
+    global memory)."""
     rng = random.Random(seed)
-    n_hosts = rng.choice([2, 3, 4]) if wide else rng.choice([1, 1, 2])
+    wide = wide or xwide
+    n_hosts = rng.choice([4, 5]) if xwide else rng.choice([2, 3, 4]) if wide else rng.choice([1, 1, 2])
     hosts, gpus_of = [], []
     for h in range(n_hosts):
         n_roots = rng.choice([1, 2, 3])
-        n_gpus = rng.choice([6, 8]) if wide else rng.choice([2, 3, 4])
+        n_gpus = 8 if xwide else rng.choice([6, 8]) if wide else rng.choice([2, 3, 4])
         roots = "\n".join(f"        - {{ id: {r * 3 + 1}, capacity_Bps: {rng.choice(['8e9', '12e9', '16e9', '24e9'])} }}"
                           for r in range(n_roots))
         gl = []
@@ -50,11 +53,11 @@ def make_scenario(seed: int, wide: bool = False) -> str:
     # tenants: pack slices per GPU without overlap
     used = {}
     tenants = []
-    n_t = rng.randint(11, 40) if wide else rng.randint(2, 7)
+    n_t = rng.randint(41, 64) if xwide else rng.randint(11, 40) if wide else rng.randint(2, 7)
     for t in range(n_t):
         for _ in range(20):
             h, g, nomig = rng.choice(gpus_of)
-            pname, pslices = rng.choice(PROFILES[:4])
+            pname, pslices = rng.choice(PROFILES[:2] if xwide else PROFILES[:4])
             first = rng.randrange(0, 7 - pslices + 1)
             occ = used.setdefault((h, g), set())
             rngs = set(range(first, first + pslices))

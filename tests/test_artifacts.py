@@ -121,7 +121,7 @@ def test_render_report_matches_reference(tmp_path):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("plan", ["e1", "e2"])
+@pytest.mark.parametrize("plan", ["e1", "e2", "e3", "llm"])
 def test_gpu_plan_artifacts_match_reference(engine, tmp_path, plan):
     """run_plan with out_dir: summary.csv and every <variant>/seed<N>/ file byte-identical to the
     reference harness; experiment.json identical except the wall-clock field."""

@@ -103,24 +103,16 @@ def test_single_replica_api(engine):
 
 
 def test_audit_invariants_hold_on_gpu_runs(engine):
-    """audit::audit_run (audit.cpp:52-122) over GPU logs == over the reference logs (both clean)."""
+    """audit::audit_run (audit.cpp:52-122), the reference's own code, over the GPU logs == over the
+    reference logs (both clean).  More cases in test_gpu_parity_wide.py."""
+    from tests._libs import ref_audit_gpu, ref_audit_ref
+
     path = GOLDEN_SCENARIOS[0]
-    lib = oracle()
-    h = lib.ref_run(scenario_json(path), None, 3, 0)
-    issues = ctypes.c_void_p()
-    n = lib.ref_result_audit(h, scenario_json(path), None, ctypes.byref(issues))
-    lib.ref_result_free(h)
-    assert n == 0
     sid = engine.load_scenario(path)
     res = engine.run_batch(sid, [3])
-    acts = res.run(0)["actions"]
+    mine = res.run(0)
     res.close()
-    last = {}
-    for a in acts:
-        if a["kind"] in ("guardrail_io_throttle", "guardrail_mps_quota", "move", "mig_up", "mig_down"):
-            if a["tenant"] in last:
-                assert a["obs_since_prev"] >= 256
-            last[a["tenant"]] = a["seq"]
+    assert ref_audit_gpu(path, mine) == ref_audit_ref(path, 3) == []
 
 
 def test_c5_64_tenants(engine):

@@ -69,6 +69,7 @@ typedef struct migsim_timing {
     double gen_ms, des_ms, select_ms, total_device_ms, wall_ms;
     int64_t replicas, tenant_ticks, completions, arrivals, events, waves;
     int64_t select_samples;  /* measurement-window latencies fed to the select kernel */
+    int64_t des_simt;        /* 1: the SIMT DES ran (one thread per replica), 0: warp per replica */
 } migsim_timing;
 
 /* per (run, tenant) flat summary row, tenants in lexicographic id order
@@ -114,6 +115,21 @@ MIGSIM_API const char* migsim_batch_run_json(migsim_batch_result* r, size_t run)
  * {tenant, seq, done_s, total_ms, compute_ms, transfer_ms, noise_ms}, tenant-major order */
 MIGSIM_API int64_t migsim_batch_completions(const migsim_batch_result* r, size_t run, double* out, int64_t cap);
 MIGSIM_API void migsim_batch_result_free(migsim_batch_result* r);
+
+/* Per-(variant, tenant) aggregates of a batch, summed over its seeds on the device -- the payload
+ * the multi-GPU reduction all-reduces (the per-variant aggregation of harness.cpp:
+ * 178-204 extended to whole distributions).  Histograms: every measurement-window latency
+ * (engine.cpp:498-502) counted in MIGSIM_HIST_BINS fixed log-spaced bins (64 per binary octave,
+ * bin 0 starting at 2^-10 ms; values below / above the range clamp into the first / last bin;
+ * edges from migsim_hist_bin_edges).  out[(v * T + t) * MIGSIM_HIST_BINS + b], tenants in
+ * lexicographic id order, variants in the batch's order.  Counts: out[(v * T + t) * 3 + k] =
+ * completed_total, completed_window, window_misses (engine.cpp:497-501). */
+#define MIGSIM_HIST_BINS 2048
+MIGSIM_API size_t migsim_batch_n_variants(const migsim_batch_result* r);
+MIGSIM_API int migsim_batch_latency_hist(const migsim_batch_result* r, uint64_t* out, size_t cap);
+MIGSIM_API int migsim_batch_tenant_counts(const migsim_batch_result* r, uint64_t* out, size_t cap);
+/* lower edge (ms) of each histogram bin; n >= MIGSIM_HIST_BINS */
+MIGSIM_API int migsim_hist_bin_edges(double* lo, size_t n);
 
 /* Standalone nearest-rank select (telemetry.cpp:38-56 / engine.cpp:800-816 semantics) over
  * n_segments host segments vals[seg_off[s] .. seg_off[s+1]); out[s * n_q + j] = quantile qs[j]. */

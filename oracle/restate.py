@@ -162,3 +162,21 @@ def confidence_interval(values: Sequence[float]) -> Tuple[float, float]:
     for v in values:
         ss += (v - mean) * (v - mean)
     return mean, 1.96 * math.sqrt(ss / n) / math.sqrt(n)
+
+
+HIST_BINS = 2048
+_HIST_SHIFT = 46
+_HIST_BASE = ((1 << 63) | ((1023 - 10) << 52)) >> _HIST_SHIFT
+
+
+def lat_bins(values):
+    """Latency-histogram bin of each FP64 value (the engine's fixed log-spaced bins: the top 18 bits
+    of the order-preserving key, 64 bins per octave from 2^-10 ms, clamped at both ends) -- a
+    numpy restatement used to bin the reference's own completion records for the histogram tests."""
+    import numpy as np
+
+    b = np.ascontiguousarray(np.asarray(values, np.float64)).view(np.uint64)
+    neg = (b >> np.uint64(63)) != 0
+    key = np.where(neg, ~b, b | np.uint64(1 << 63))
+    v = (key >> np.uint64(_HIST_SHIFT)).astype(np.int64)
+    return np.clip(v - _HIST_BASE, 0, HIST_BINS - 1)

@@ -70,6 +70,7 @@ class _Timing(ctypes.Structure):
         ("events", ctypes.c_int64),
         ("waves", ctypes.c_int64),
         ("select_samples", ctypes.c_int64),
+        ("des_simt", ctypes.c_int64),
     ]
 
 
@@ -154,6 +155,11 @@ def load_library() -> ctypes.CDLL:
     lib.migsim_gpu_admit.argtypes = [vp, ctypes.c_int32, sz] + [vp] * 11 + [ctypes.POINTER(ctypes.c_double), cp, sz]
     lib.migsim_free.argtypes = [vp]
     lib.migsim_scenario_dump.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
+    lib.migsim_batch_n_variants.argtypes = [vp]
+    lib.migsim_batch_n_variants.restype = sz
+    lib.migsim_batch_latency_hist.argtypes = [vp, vp, sz]
+    lib.migsim_batch_tenant_counts.argtypes = [vp, vp, sz]
+    lib.migsim_hist_bin_edges.argtypes = [vp, sz]
     _lib_handle = lib
     return lib
 
@@ -170,6 +176,15 @@ def _check(code: int, err: ctypes.Array) -> None:
 
 
 KEEP_INT = -(2 ** 31)  # MIGSIM_KEEP_INT (include/migsim_b200.h)
+HIST_BINS = 2048  # MIGSIM_HIST_BINS
+
+
+def hist_bin_edges() -> np.ndarray:
+    """Lower edge (ms) of each latency-histogram bin (64 bins per binary octave from 2^-10 ms)."""
+    lo = np.zeros(HIST_BINS, dtype=np.float64)
+    if load_library().migsim_hist_bin_edges(lo.ctypes.data, HIST_BINS) != 0:
+        raise RuntimeError("migsim_hist_bin_edges failed")
+    return lo
 
 
 @dataclass
@@ -236,6 +251,26 @@ class BatchResult:
             s = self._engine._lib.migsim_batch_run_json(self._handle, i)
             self._json_cache[i] = json.loads(s.decode())
         return self._json_cache[i]
+
+    def latency_hist(self) -> np.ndarray:
+        """int64 [n_variants, n_tenants, HIST_BINS]: every measurement-window latency of every seed,
+        binned (hist_bin_edges()) and summed per (variant, tenant) on the device."""
+        lib = self._engine._lib
+        nv = lib.migsim_batch_n_variants(self._handle)
+        out = np.zeros((nv, self.n_tenants, HIST_BINS), dtype=np.uint64)
+        if lib.migsim_batch_latency_hist(self._handle, out.ctypes.data, out.size) != 0:
+            raise RuntimeError("migsim_batch_latency_hist failed")
+        return out.astype(np.int64)
+
+    def tenant_counts(self) -> np.ndarray:
+        """int64 [n_variants, n_tenants, 3]: completed_total, completed_window, window_misses summed
+        over the batch's seeds (engine.cpp:497-501)."""
+        lib = self._engine._lib
+        nv = lib.migsim_batch_n_variants(self._handle)
+        out = np.zeros((nv, self.n_tenants, 3), dtype=np.uint64)
+        if lib.migsim_batch_tenant_counts(self._handle, out.ctypes.data, out.size) != 0:
+            raise RuntimeError("migsim_batch_tenant_counts failed")
+        return out.astype(np.int64)
 
     def completions(self, i: int) -> np.ndarray:
         """Per-completion records [n, 7] = tenant, seq, done_s, total, compute, transfer, noise."""

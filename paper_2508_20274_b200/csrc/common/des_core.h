@@ -255,14 +255,22 @@ MG_HD int __popcll_hd(uint64_t m) {
 #endif
 }
 
-MG_HD void hist_add(uint32_t* p) {
+// per_thread: the replica is run by this thread alone (SIMT kernel, host harness); otherwise the
+// handlers run warp-uniformly (every lane executes them) and one lane counts.
+MG_HD void hist_add(uint32_t* p, bool per_thread = false) {
 #if defined(__CUDA_ARCH__)
-    // the handlers run warp-uniformly (every lane executes them): one lane counts
-    if ((threadIdx.x & 31) == 0) atomicAdd(p, 1u);  // result unused: a fire-and-forget RED
+    if (per_thread || (threadIdx.x & 31) == 0) atomicAdd(p, 1u);  // result unused: a fire-and-forget RED
 #else
+    (void)per_thread;
     *p += 1;
 #endif
 }
+
+// Execution model of a Lanes type: kPerThread = one thread runs one replica (no warp redundancy).
+template <class Lanes>
+struct LanesTraits {
+    static constexpr bool kPerThread = false;
+};
 
 MG_HD void prefetch_l1(const void* p) {
 #if defined(__CUDA_ARCH__)
@@ -691,7 +699,8 @@ struct Sim {
             if (total < d.win_min) d.win_min = total;
             if (total > d.win_max) d.win_max = total;
             if (total > spec(i).slo_tail_ms) d.misses += 1;
-            if (io.win_hist) hist_add(io.win_hist + static_cast<int64_t>(i) * kHistBins + lat_bin(total));
+            if (io.win_hist)
+                hist_add(io.win_hist + static_cast<int64_t>(i) * kHistBins + lat_bin(total), LanesTraits<Lanes>::kPerThread);
         }
         if (io.c_total) {
             const int64_t o = base + static_cast<int64_t>(idx);

@@ -40,6 +40,9 @@ struct ParityGuard : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
+// batches with at least this many replicas run the SIMT DES (one thread per replica)
+constexpr size_t kSimtMinJobs = 4096;
+
 #define CK(x)                                                                                          \
     do {                                                                                               \
         cudaError_t e_ = (x);                                                                          \
@@ -112,6 +115,7 @@ struct WaveAlloc {
     DevBuf<mg::FabricRow> tr_fab;
     DevBuf<mg::TailWin> tr_win;
     DevBuf<uint32_t> win_hist;
+    DevBuf<unsigned long long> hist_sum;  // [n_var][T][kHistBins] over all waves of a batch
     DevBuf<double> tr_ring;
     DevBuf<mg::PScenario> scen;
     DevBuf<mg::PController> ctrl;
@@ -153,6 +157,8 @@ struct migsim_batch_result {
     std::vector<int64_t> comp_off;
     std::vector<std::string> json;
     std::vector<mgb::TraceRows> traces;  // per run, with write_traces
+    std::vector<uint64_t> hist;          // [n_var][T][kHistBins] window-latency histograms (lat_hist.h bins)
+    std::vector<uint64_t> counts;        // [n_var][T][3] completed_total, completed_window, window_misses
     migsim_timing timing{};
 };
 
@@ -181,7 +187,16 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     // working-set layout: controller rings in shared memory when a replica stays under 96 KB
     const int G = P.scen.n_gpus, I = P.scen.n_irq, H = P.scen.n_hosts;
     mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true, G, I, H);
-    const bool rings_in_smem = L.total <= 96 * 1024;
+    // DES form: SIMT (one thread per replica) for large batches, warp-per-replica otherwise
+    // (MIGSIM_DES=warp|simt overrides)
+    const mg::SimtLayout Y = mg::simt_layout(T, R, G, I, H, static_cast<int>(n_var));
+    const char* des_env = std::getenv("MIGSIM_DES");
+    const std::string des_mode = des_env ? des_env : "auto";
+    int simt_lanes = mg::kSimtBlock;
+    while (simt_lanes > 1 && Y.bytes(simt_lanes) > 200 * 1024) simt_lanes /= 2;
+    const bool simt_fits = T <= mg::kSimtMaxTenants && Y.bytes(1) <= 200 * 1024;
+    const bool use_simt = simt_fits && (des_mode == "simt" || (des_mode == "auto" && n_jobs >= kSimtMinJobs));
+    const bool rings_in_smem = !use_simt && L.total <= 96 * 1024;
     if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false, G, I, H);
     // wave size from free memory
     const size_t per_rep = static_cast<size_t>(P.cap_sum) * 8 * (8 + (keep ? 5 : 0)) + static_cast<size_t>(T) * 8 +
@@ -256,7 +271,9 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     A.pause_off.alloc(W + 1);
     A.scen.alloc(1);
     A.ctrl.alloc(n_var);
+    A.hist_sum.alloc(n_var * T * mg::kHistBins);
     cudaStream_t s = g->stream;
+    CK(cudaMemsetAsync(A.hist_sum.p, 0, sizeof(unsigned long long) * n_var * T * mg::kHistBins, s));
     CK(cudaMemcpyAsync(A.scen.p, &P.scen, sizeof(mg::PScenario), cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(A.ctrl.p, P.ctrl.data(), sizeof(mg::PController) * n_var, cudaMemcpyHostToDevice, s));
     CK(cudaMemcpyAsync(A.off.p, P.off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
@@ -311,6 +328,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     B.rings_in_smem = rings_in_smem;
     B.dwell = P.max_dwell;
     B.validation = P.max_validation;
+    B.n_variants = static_cast<int32_t>(n_var);
     DevBuf<unsigned long long> prof;
     const bool want_prof = std::getenv("MIGSIM_PROFILE_EVENTS") != nullptr;
     if (want_prof) {
@@ -320,7 +338,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     }
 
     auto* des = T <= mg::kRegSlotMaxTenants ? mg::des_kernel_reg : mg::des_kernel;
-    CK(cudaFuncSetAttribute(des, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+    if (use_simt)
+        CK(cudaFuncSetAttribute(mg::des_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(Y.bytes(simt_lanes))));
+    else
+        CK(cudaFuncSetAttribute(des, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
     const size_t sel_smem = mg::select_smem_bytes();
     CK(cudaFuncSetAttribute(mg::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sel_smem)));
     const size_t cl_smem = mg::select_cluster_smem_bytes();
@@ -363,7 +385,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         mg::gen_marks_kernel<<<static_cast<unsigned>(4 * nt), 32, 0, s>>>(A.scen.p, B, w);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[1], s));
-        des<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
+        if (use_simt)
+            mg::des_simt_kernel<<<static_cast<unsigned>((w + simt_lanes - 1) / simt_lanes), simt_lanes,
+                                  static_cast<size_t>(Y.bytes(simt_lanes)), s>>>(A.scen.p, A.ctrl.p, B, w, Y);
+        else
+            des<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[2], s));
         if (sel_cluster)
@@ -373,6 +399,12 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
             mg::WaveBuffers Bs = B;
             if (sel_two_pass) Bs.win_hist = nullptr;
             mg::select_kernel<<<static_cast<unsigned>(nt), mg::select_threads(), sel_smem, s>>>(Bs, T, w);
+        }
+        {
+            constexpr int kChunk = 256;
+            const dim3 grid(static_cast<unsigned>((T * mg::kHistBins + 255) / 256),
+                            static_cast<unsigned>((w + kChunk - 1) / kChunk));
+            mg::hist_reduce_kernel<<<grid, 256, 0, s>>>(A.win_hist.p, A.variant.p, w, T, kChunk, A.hist_sum.p);
         }
         CK(cudaGetLastError());
         CK(cudaEventRecord(g->ev[3], s));
@@ -480,6 +512,20 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
             }
         }
     }
+    res.hist.resize(n_var * T * mg::kHistBins);
+    CK(cudaMemcpyAsync(res.hist.data(), A.hist_sum.p, sizeof(uint64_t) * res.hist.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    res.counts.assign(n_var * T * 3, 0);
+    for (size_t job = 0; job < n_jobs; ++job) {
+        const size_t v = job / seeds.size();
+        for (int i = 0; i < T; ++i) {
+            const mg::TenantOut& o = res.tout[job * T + i];
+            uint64_t* c = res.counts.data() + (v * T + i) * 3;
+            c[0] += o.completed_total;
+            c[1] += o.completed_window;
+            c[2] += o.window_misses;
+        }
+    }
     res.json.assign(n_jobs, std::string());
     res.timing.gen_ms = gen_ms;
     res.timing.des_ms = des_ms;
@@ -492,6 +538,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.timing.events = events;
     res.timing.waves = waves;
     res.timing.select_samples = samples;
+    res.timing.des_simt = use_simt ? 1 : 0;
     res.timing.wall_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
 }
@@ -720,6 +767,29 @@ int64_t migsim_batch_completions(const migsim_batch_result* r, size_t run, doubl
 }
 
 void migsim_batch_result_free(migsim_batch_result* r) { delete r; }
+
+size_t migsim_batch_n_variants(const migsim_batch_result* r) { return r ? r->variants.size() : 0; }
+
+int migsim_batch_latency_hist(const migsim_batch_result* r, uint64_t* out, size_t cap) {
+    if (!r || !out || cap < r->hist.size()) return MIGSIM_ERR_RUNTIME;
+    std::memcpy(out, r->hist.data(), sizeof(uint64_t) * r->hist.size());
+    return MIGSIM_OK;
+}
+
+int migsim_batch_tenant_counts(const migsim_batch_result* r, uint64_t* out, size_t cap) {
+    if (!r || !out || cap < r->counts.size()) return MIGSIM_ERR_RUNTIME;
+    std::memcpy(out, r->counts.data(), sizeof(uint64_t) * r->counts.size());
+    return MIGSIM_OK;
+}
+
+int migsim_hist_bin_edges(double* lo, size_t n) {
+    if (!lo || n < static_cast<size_t>(mg::kHistBins)) return MIGSIM_ERR_RUNTIME;
+    for (int b = 0; b < mg::kHistBins; ++b) {
+        const uint64_t bits = mg::lat_bin_lo(static_cast<uint32_t>(b)) & ~(1ull << 63);  // positive values
+        std::memcpy(lo + b, &bits, 8);
+    }
+    return MIGSIM_OK;
+}
 
 int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_t* seg_off, size_t n_segments, const double* qs,
                       size_t n_q, double* out, double* device_ms, char* err, size_t errlen) {

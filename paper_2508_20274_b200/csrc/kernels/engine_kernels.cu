@@ -195,41 +195,23 @@ __device__ __forceinline__ bool next_event<HostLanes>(Sim<HostLanes>& sim, int T
     return true;
 }
 
-template <class Lanes>
-__device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const PController* __restrict__ C,
-                                         const WaveBuffers& B, int n_rep, const SimLayout& L) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int r = blockIdx.x;
-    if (r >= n_rep) return;
-    const int T = S->n_tenants;
-    const int lane = threadIdx.x;
-    // read-only scenario tables -> shared memory (cooperative 8-B copies; all PODs are 8-B multiples)
-    auto copy16 = [&](int64_t dst_off, const void* src, int64_t bytes) {
+// read-only scenario tables -> shared memory (cooperative 8-B copies; all PODs are 8-B multiples)
+__device__ __forceinline__ void copy_tables(unsigned char* smem, const SimLayout& L, const PScenario* __restrict__ S,
+                                            int tid, int nthreads) {
+    auto copy8 = [&](int64_t dst_off, const void* src, int64_t bytes) {
         const uint64_t* s8 = reinterpret_cast<const uint64_t*>(src);
         uint64_t* d8 = reinterpret_cast<uint64_t*>(smem + dst_off);
-        for (int64_t k = lane; k < bytes / 8; k += 32) d8[k] = s8[k];
+        for (int64_t k = tid; k < bytes / 8; k += nthreads) d8[k] = s8[k];
     };
-    copy16(L.sc_tn, S->tenants, static_cast<int64_t>(sizeof(PTenant)) * T);
-    copy16(L.sc_gp, S->gpus, static_cast<int64_t>(sizeof(PGpu)) * S->n_gpus);
-    copy16(L.sc_rt, S->roots, static_cast<int64_t>(sizeof(PRoot)) * S->n_roots);
-    copy16(L.sc_iq, S->irq, static_cast<int64_t>(sizeof(PIrq)) * S->n_irq);
-    copy16(L.sc_hio, S->host_io_capacity, align16(8ll * S->n_hosts));
-    copy16(L.sc_ctrl, C + B.variant[r], static_cast<int64_t>(sizeof(PController)));
-    __syncwarp();
-    const PController& Cv = *reinterpret_cast<const PController*>(smem + L.sc_ctrl);
-    SimState& st = *reinterpret_cast<SimState*>(smem + L.st);
-    TenantDyn* td = reinterpret_cast<TenantDyn*>(smem + L.td);
-    TenantCtl* ctl = reinterpret_cast<TenantCtl*>(smem + L.ctl);
-    RootDyn* rd = reinterpret_cast<RootDyn*>(smem + L.rd);
-    double* win;
-    double* vwin;
-    if (B.rings_in_smem) {
-        win = reinterpret_cast<double*>(smem + L.win);
-        vwin = reinterpret_cast<double*>(smem + L.vwin);
-    } else {
-        win = B.rings + static_cast<int64_t>(r) * T * (B.dwell + B.validation);
-        vwin = win + static_cast<int64_t>(T) * B.dwell;
-    }
+    copy8(L.sc_tn, S->tenants, static_cast<int64_t>(sizeof(PTenant)) * S->n_tenants);
+    copy8(L.sc_gp, S->gpus, static_cast<int64_t>(sizeof(PGpu)) * S->n_gpus);
+    copy8(L.sc_rt, S->roots, static_cast<int64_t>(sizeof(PRoot)) * S->n_roots);
+    copy8(L.sc_iq, S->irq, static_cast<int64_t>(sizeof(PIrq)) * S->n_irq);
+    copy8(L.sc_hio, S->host_io_capacity, align16(8ll * S->n_hosts));
+}
+
+// global-memory side of replica r (arrival records, scratch, outputs)
+__device__ __forceinline__ ReplicaIO replica_io(const WaveBuffers& B, const PScenario* __restrict__ S, int r, int T) {
     const int64_t base = static_cast<int64_t>(r) * B.cap_sum;
     ReplicaIO io;
     io.arr_t = B.arr_t + base;
@@ -271,6 +253,39 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
         io.tr_fab = nullptr;
         io.tr_win = nullptr;
     }
+    return io;
+}
+
+template <class Lanes>
+__device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const PController* __restrict__ C,
+                                         const WaveBuffers& B, int n_rep, const SimLayout& L) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int r = blockIdx.x;
+    if (r >= n_rep) return;
+    const int T = S->n_tenants;
+    const int lane = threadIdx.x;
+    copy_tables(smem, L, S, lane, 32);
+    {
+        const uint64_t* s8 = reinterpret_cast<const uint64_t*>(C + B.variant[r]);
+        uint64_t* d8 = reinterpret_cast<uint64_t*>(smem + L.sc_ctrl);
+        for (int k = lane; k < static_cast<int>(sizeof(PController) / 8); k += 32) d8[k] = s8[k];
+    }
+    __syncwarp();
+    const PController& Cv = *reinterpret_cast<const PController*>(smem + L.sc_ctrl);
+    SimState& st = *reinterpret_cast<SimState*>(smem + L.st);
+    TenantDyn* td = reinterpret_cast<TenantDyn*>(smem + L.td);
+    TenantCtl* ctl = reinterpret_cast<TenantCtl*>(smem + L.ctl);
+    RootDyn* rd = reinterpret_cast<RootDyn*>(smem + L.rd);
+    double* win;
+    double* vwin;
+    if (B.rings_in_smem) {
+        win = reinterpret_cast<double*>(smem + L.win);
+        vwin = reinterpret_cast<double*>(smem + L.vwin);
+    } else {
+        win = B.rings + static_cast<int64_t>(r) * T * (B.dwell + B.validation);
+        vwin = win + static_cast<int64_t>(T) * B.dwell;
+    }
+    const ReplicaIO io = replica_io(B, S, r, T);
     Sim<Lanes> sim(*S, Cv, io, st, make_lanes<Lanes>(smem, L, T), td, ctl, rd);
     sim.tn = reinterpret_cast<const PTenant*>(smem + L.sc_tn);
     sim.gp = reinterpret_cast<const PGpu*>(smem + L.sc_gp);
@@ -339,6 +354,112 @@ __global__ void MG_DES_BOUNDS des_kernel_reg(const PScenario* __restrict__ S,
 }
 
 // ---------------------------------------------------------------------------------------------
+// replica DES, SIMT form: one THREAD per replica.
+//
+// The warp kernels above run one replica per warp with every lane repeating the scalar handler
+// work.  Here each lane owns a replica: its working set (SimState, TenantDyn/Ctl, RootDyn, event
+// slots) lives in a private shared-memory slab at a stride that is an odd multiple of 8 bytes, so
+// the 32 lanes' same-field loads hit 32 distinct bank pairs; the controller rings go to global
+// memory.  Lanes diverge by event kind, so one pass of the warp executes each kind's handler once
+// for all lanes that drew that kind -- per event, an order of magnitude fewer issued instructions
+// than the warp-redundant form.  The scenario tables and every variant's PController are staged
+// once per block.  Used for large waves (the saturated regime); small waves keep the warp kernel,
+// whose lane-parallel argmin gives lower per-replica latency.
+struct SimtLanes {
+    Slot* slots;  // this thread's 5T+1 slots
+    __device__ __forceinline__ void set(int s, double t, uint64_t key) {
+        slots[s].t = t;
+        slots[s].key = key;
+    }
+    __device__ __forceinline__ void clear(int s) {
+        slots[s].t = k_inf();
+        slots[s].key = ~0ull;
+    }
+};
+template <>
+struct MaskOf<SimtLanes> {
+    using type = uint32_t;  // T <= kSimtMaxTenants
+};
+template <>
+struct LanesTraits<SimtLanes> {
+    static constexpr bool kPerThread = true;
+};
+
+__global__ void __launch_bounds__(kSimtBlock) des_simt_kernel(const PScenario* __restrict__ S,
+                                                              const PController* __restrict__ C, WaveBuffers B,
+                                                              int n_rep, SimtLayout Y) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int tid = threadIdx.x;
+    copy_tables(smem, Y.tab, S, tid, blockDim.x);
+    {
+        const uint64_t* s8 = reinterpret_cast<const uint64_t*>(C);
+        uint64_t* d8 = reinterpret_cast<uint64_t*>(smem + Y.ctrl);
+        const int n8 = B.n_variants * static_cast<int>(sizeof(PController) / 8);
+        for (int k = tid; k < n8; k += blockDim.x) d8[k] = s8[k];
+    }
+    __syncthreads();
+    const int r = blockIdx.x * blockDim.x + tid;
+    if (r >= n_rep) return;
+    const int T = S->n_tenants;
+    unsigned char* ln = smem + Y.lanes + static_cast<int64_t>(tid) * Y.stride;
+    const SimLayout& L = Y.lane;
+    const PController& Cv = reinterpret_cast<const PController*>(smem + Y.ctrl)[B.variant[r]];
+    SimState& st = *reinterpret_cast<SimState*>(ln + L.st);
+    TenantDyn* td = reinterpret_cast<TenantDyn*>(ln + L.td);
+    TenantCtl* ctl = reinterpret_cast<TenantCtl*>(ln + L.ctl);
+    RootDyn* rd = reinterpret_cast<RootDyn*>(ln + L.rd);
+    double* win = B.rings + static_cast<int64_t>(r) * T * (B.dwell + B.validation);
+    double* vwin = win + static_cast<int64_t>(T) * B.dwell;
+    const ReplicaIO io = replica_io(B, S, r, T);
+    Sim<SimtLanes> sim(*S, Cv, io, st, SimtLanes{reinterpret_cast<Slot*>(ln + L.slots)}, td, ctl, rd);
+    sim.tn = reinterpret_cast<const PTenant*>(smem + Y.tab.sc_tn);
+    sim.gp = reinterpret_cast<const PGpu*>(smem + Y.tab.sc_gp);
+    sim.rt = reinterpret_cast<const PRoot*>(smem + Y.tab.sc_rt);
+    sim.iq = reinterpret_cast<const PIrq*>(smem + Y.tab.sc_iq);
+    sim.hio = reinterpret_cast<const double*>(smem + Y.tab.sc_hio);
+    sim.init(B.file_order, win, vwin);
+    const double duration = S->duration_s;
+    const Slot* slots = sim.lanes.slots;
+    const int nhot = 3 * T + 1;
+    for (;;) {
+        // this replica's next event: linear argmin over its live slots in (t, kind, seq) order;
+        // t >= 0, so the IEEE bits order as unsigned and (t_bits, key) compares lexicographically
+        const int n = sim.any_rare() ? kEvKinds * T + 1 : nhot;
+        uint64_t bt = ~0ull, bk = ~0ull;
+        int bs = -1;
+        for (int k = 0; k < n; ++k) {
+            const uint64_t kk = slots[k].key;
+            const uint64_t tb = static_cast<uint64_t>(__double_as_longlong(slots[k].t));
+            if (kk != ~0ull && (tb < bt || (tb == bt && kk < bk))) {
+                bt = tb;
+                bk = kk;
+                bs = k;
+            }
+        }
+        if (bs < 0) break;
+        const double t = __longlong_as_double(static_cast<long long>(bt));
+        if (t > duration) break;  // engine.cpp:872
+        const int kind = static_cast<int>(bk >> 48);
+        sim.lanes.clear(bs);
+        sim.dispatch(kind, sim.slot_tenant(kind, bs), t);
+    }
+    sim.now = duration;
+    sim.finish();
+}
+
+SimtLayout simt_layout(int T, int R, int G, int I, int H, int n_variants) {
+    SimtLayout Y;
+    Y.tab = sim_layout(T, R, 0, 0, false, G, I, H);
+    Y.ctrl = Y.tab.sc_ctrl;  // the per-variant controllers replace the single staged one
+    Y.lanes = align16(Y.ctrl + static_cast<int64_t>(sizeof(PController)) * n_variants);
+    Y.lane = sim_layout(T, R, 0, 0, false);  // G = 0: per-lane part only, st at offset 0
+    int64_t stride = (Y.lane.total + 7) & ~static_cast<int64_t>(7);
+    if (((stride / 8) & 1) == 0) stride += 8;  // odd multiple of 8 B: conflict-free same-field access
+    Y.stride = stride;
+    return Y;
+}
+
+// ---------------------------------------------------------------------------------------------
 __global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,
                                        const int64_t* __restrict__ dst_off, ActionRec* __restrict__ dst, int n_rep) {
     const int r = blockIdx.x;
@@ -363,5 +484,33 @@ __global__ void libm_kernel(int fn, const double* __restrict__ x, const double* 
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     out[i] = fn == 0 ? gl_log(x[i]) : fn == 1 ? gl_exp(x[i]) : gl_pow(x[i], y[i]);
+}
+}  // namespace mg
+
+namespace mg {
+// ---------------------------------------------------------------------------------------------
+// Per-(variant, tenant) latency histograms of a wave: sum the DES's per-(replica, tenant) window
+// histograms (lat_hist.h bins) over replicas into int64 accumulators [n_var][T][kHistBins] that
+// persist across waves -- the payload the multi-GPU reduction all-reduces.
+// Thread = one (tenant, bin); blockIdx.y = a chunk of replicas; replicas are variant-major, so a
+// thread flushes its running sum whenever the variant changes (few atomics, coalesced reads).
+__global__ void hist_reduce_kernel(const uint32_t* __restrict__ win_hist, const int32_t* __restrict__ variant,
+                                   int n_rep, int T, int chunk, unsigned long long* __restrict__ out) {
+    const int tb = blockIdx.x * blockDim.x + threadIdx.x;  // t * kHistBins + bin
+    if (tb >= T * kHistBins) return;
+    const int r0 = blockIdx.y * chunk;
+    const int r1 = min(n_rep, r0 + chunk);
+    unsigned long long acc = 0;
+    int v = r0 < r1 ? variant[r0] : 0;
+    for (int r = r0; r < r1; ++r) {
+        const int vr = variant[r];
+        if (vr != v) {
+            if (acc) atomicAdd(out + (static_cast<int64_t>(v) * T * kHistBins + tb), acc);
+            acc = 0;
+            v = vr;
+        }
+        acc += win_hist[static_cast<int64_t>(r) * T * kHistBins + tb];
+    }
+    if (acc) atomicAdd(out + (static_cast<int64_t>(v) * T * kHistBins + tb), acc);
 }
 }  // namespace mg

@@ -47,6 +47,7 @@ struct WaveBuffers {
     int32_t action_cap, pause_cap;
     int32_t any_irq_noise, rings_in_smem;
     int32_t dwell, validation;  // ring strides (max over variants)
+    int32_t n_variants, pad_v;  // PController entries at C
     unsigned long long* prof;   // [6][3] event-loop cycle counters (MG_PROFILE_EVENTS builds only)
 };
 
@@ -58,7 +59,24 @@ __global__ void des_kernel(const PScenario* __restrict__ S, const PController* _
 constexpr int kRegSlotMaxTenants = 10;  // 3T+1 hot slots and 2T rare slots within 32 lanes
 __global__ void des_kernel_reg(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
                                int n_rep, SimLayout L);
+// SIMT form: one thread per replica, for large waves (see engine_kernels.cu)
+constexpr int kSimtMaxTenants = 32;  // 32-bit tenant masks
+constexpr int kSimtBlock = 32;       // threads (replicas) per block, at most
+struct SimtLayout {
+    SimLayout tab;   // block-shared scenario tables (sc_* offsets)
+    SimLayout lane;  // per-replica working set, offsets inside one lane's slab
+    int64_t ctrl;    // PController[n_variants]
+    int64_t lanes;   // first lane slab
+    int64_t stride;  // bytes per lane slab (odd multiple of 8)
+    int64_t bytes(int lanes_per_block) const { return lanes + stride * lanes_per_block; }
+};
+SimtLayout simt_layout(int T, int R, int G, int I, int H, int n_variants);
+__global__ void des_simt_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
+                                int n_rep, SimtLayout Y);
 __global__ void select_kernel(WaveBuffers B, int T, int n_rep);
+// per-(variant, tenant) latency histograms summed over a wave's replicas (int64, persistent)
+__global__ void hist_reduce_kernel(const uint32_t* __restrict__ win_hist, const int32_t* __restrict__ variant,
+                                   int n_rep, int T, int chunk, unsigned long long* __restrict__ out);
 // same results, one HBM pass: 4-CTA cluster per segment, TMA bulk loads, DSMEM histogram/gather
 __global__ void select_cluster_kernel(WaveBuffers B, int T, int n_rep);
 __global__ void compact_actions_kernel(const ActionRec* __restrict__ src, int cap, const ReplicaOut* __restrict__ rout,

@@ -228,3 +228,18 @@ def test_capi_error_codes_without_gpu():
 
     with _pt.raises(ConfigError):
         scenario_spec("/nonexistent/scenario.yaml")
+
+
+def test_hist_bin_edges_match_restated_bins():
+    """migsim_hist_bin_edges (host-only ABI) gives each bin's lower edge: the edge falls in its bin,
+    the value just below it in the previous bin (restated binning, oracle/restate.lat_bins)."""
+    from oracle import restate
+    from paper_2508_20274_b200.api import HIST_BINS, hist_bin_edges
+
+    lo = hist_bin_edges()
+    assert len(lo) == HIST_BINS and lo[0] == 2.0 ** -10 and (np.diff(lo) > 0).all()
+    assert (restate.lat_bins(lo) == np.arange(HIST_BINS)).all()
+    below = np.nextafter(lo[1:], 0)
+    assert (restate.lat_bins(below) == np.arange(HIST_BINS - 1)).all()
+    # octave structure: 64 bins per doubling
+    assert lo[64] == 2.0 ** -9 and lo[640] == 1.0

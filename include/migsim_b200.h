@@ -70,6 +70,11 @@ typedef struct migsim_timing {
     int64_t replicas, tenant_ticks, completions, arrivals, events, waves;
     int64_t select_samples;  /* measurement-window latencies fed to the select kernel */
     int64_t des_simt;        /* 1: the SIMT DES ran (one thread per replica), 0: warp per replica */
+    int64_t des_blocks_per_sm; /* occupancy of the DES launch (resident blocks per SM) */
+    int64_t des_smem_bytes;    /* dynamic shared memory per DES block */
+    int64_t kernel_launches;   /* engine kernels launched by the call */
+    int64_t h2d_bytes, d2h_bytes; /* host<->device bytes copied by the call */
+    int64_t pipeline_slots;       /* 2: waves double-buffered on two streams (total_device_ms = span) */
 } migsim_timing;
 
 /* per (run, tenant) flat summary row, tenants in lexicographic id order
@@ -86,6 +91,87 @@ MIGSIM_API void migsim_gpu_close(migsim_gpu* g);
 MIGSIM_API int migsim_gpu_load_scenario(migsim_gpu* g, const char* yaml_text, const char* source_name, int32_t* scenario_id,
                              char* err, size_t errlen);
 MIGSIM_API int migsim_gpu_load_scenario_file(migsim_gpu* g, const char* path, int32_t* scenario_id, char* err, size_t errlen);
+/* ---- in-memory scenario specs ----------------------------------------------------------
+ * Plain-C mirror of scenario::ScenarioSpec (scenario.hpp:30-61) with its model/workload parts
+ * (TopologySpec/HostSpec/GpuSpec/PcieRootSpec model.hpp:74-105, TenantSpec model.hpp:122-139,
+ * ControllerConfig model.hpp:186-224, InterferenceSchedule workload.hpp:56-74), presets already
+ * applied, every field explicit.  Tenants, hosts, GPUs and roots in the spec's own order.  This is
+ * how a spec the caller built or mutated in memory (e.g. harness::apply_variant, the e3 sweep's
+ * ControllerConfig edits, harness.cpp:89-110) crosses the ABI without a YAML round trip; the
+ * engine copies it, runs ScenarioSpec::validate (scenario.cpp:270-313 checks) and canonicalises
+ * the orders itself. */
+typedef struct migsim_schedule_desc {
+    int32_t kind; /* 0 always, 1 square_wave, 2 phases */
+    double period_s, duty, offset_s;
+    const double* phase_start_s; /* [n_phases] */
+    const double* phase_end_s;   /* [n_phases] */
+    size_t n_phases;
+} migsim_schedule_desc;
+typedef struct migsim_gpu_desc {
+    int32_t id, pcie_root_id, numa_id, core_group, total_slices, mig_enabled;
+} migsim_gpu_desc;
+typedef struct migsim_root_desc {
+    int32_t id;
+    double capacity_Bps;
+} migsim_root_desc;
+typedef struct migsim_host_desc {
+    const migsim_gpu_desc* gpus;
+    size_t n_gpus;
+    int32_t numa_domains;
+    const migsim_root_desc* roots;
+    size_t n_roots;
+    const int32_t* irq_hot_core_groups;
+    size_t n_irq_hot;
+    double io_capacity_Bps;
+} migsim_host_desc;
+typedef struct migsim_tenant_desc {
+    const char* id;
+    int32_t tclass; /* 0 latency_sensitive, 1 bandwidth_heavy, 2 compute_heavy */
+    double arrival_rate_hz, arrival_cv;
+    const double* mix_bytes;  /* transfer_mix, [n_mix] */
+    const double* mix_weight; /* [n_mix] */
+    size_t n_mix;
+    double base_compute_ms, service_cv, slo_tail_ms, weight, pcie_cap_Bps, host_io_Bps, sm_demand, noise_mean_ms;
+    int32_t host, gpu, first_slice, slice_count; /* TenantEntry::placement */
+    const char* profile;                         /* TenantEntry::profile_name, e.g. "2g" */
+    migsim_schedule_desc schedule;
+} migsim_tenant_desc;
+typedef struct migsim_irq_desc {
+    int32_t host, core_group;
+    double extra_noise_ms;
+    migsim_schedule_desc schedule;
+} migsim_irq_desc;
+typedef struct migsim_controller_desc {
+    int32_t enabled, enable_mig, enable_placement, enable_guardrails;
+    double tail_threshold_ms;
+    int32_t persistence_windows, dwell_obs, cooldown_obs;
+    double sample_interval_s, warmup_s, move_futility_ratio, throttle_duration_s, quota_duration_s, ema_alpha,
+        hysteresis_clear_ratio, relax_stability_ratio, relax_score_threshold;
+    int32_t validation_obs;
+    double rollback_regress_ratio, diag_pcie_util_threshold, diag_host_io_threshold, diag_sm_util_threshold,
+        move_margin;
+    int32_t admission_queue_timeout_epochs;
+    double guardrail_io_throttle_Bps, guardrail_mps_quota_pct, irq_lookback_s, throughput_floor;
+} migsim_controller_desc;
+typedef struct migsim_scenario_desc {
+    const char* name;
+    double duration_s, measure_start_s;
+    int32_t fabric_redistribute;
+    const migsim_host_desc* hosts;
+    size_t n_hosts;
+    const migsim_tenant_desc* tenants;
+    size_t n_tenants;
+    const migsim_irq_desc* irq_bursts;
+    size_t n_irq_bursts;
+    migsim_controller_desc controller;
+} migsim_scenario_desc;
+/* load an in-memory spec; same ids and errors as migsim_gpu_load_scenario (code 1 = ConfigError
+ * from ScenarioSpec::validate, message prefixed "<spec>") */
+MIGSIM_API int migsim_gpu_load_spec(migsim_gpu* g, const migsim_scenario_desc* spec, int32_t* scenario_id, char* err,
+                                    size_t errlen);
+/* drop a loaded scenario's host copy (its id is not reused; later use is a config error) */
+MIGSIM_API int migsim_gpu_release_scenario(migsim_gpu* g, int32_t scenario_id);
+
 /* canonical tenant order of a loaded scenario: writes the i-th id (lexicographic) */
 MIGSIM_API int migsim_scenario_n_tenants(migsim_gpu* g, int32_t scenario_id);
 MIGSIM_API int migsim_scenario_tenant_id(migsim_gpu* g, int32_t scenario_id, int32_t i, char* buf, size_t buflen);
@@ -114,6 +200,17 @@ MIGSIM_API const char* migsim_batch_run_json(migsim_batch_result* r, size_t run)
 /* per-completion records of one run (only with keep_completions): 7 doubles per completion
  * {tenant, seq, done_s, total_ms, compute_ms, transfer_ms, noise_ms}, tenant-major order */
 MIGSIM_API int64_t migsim_batch_completions(const migsim_batch_result* r, size_t run, double* out, int64_t cap);
+/* engine::CompletionRecord (engine.hpp:44-54) of one run, only with keep_completions: in the
+ * reference's RunResult::completions order (completion order, engine.cpp:504); tenant = canonical
+ * (lexicographic) index, seq = the tenant's request sequence number (engine.cpp:425,482).  Returns
+ * the record count (out may be NULL to query it), -1 without keep_completions. */
+typedef struct migsim_completion {
+    int32_t tenant, pad;
+    uint64_t seq;
+    double arrived_s, done_s, total_ms, compute_ms, transfer_ms, noise_ms, transfer_bytes;
+} migsim_completion;
+MIGSIM_API int64_t migsim_batch_completion_records(const migsim_batch_result* r, size_t run, migsim_completion* out,
+                                                   int64_t cap);
 MIGSIM_API void migsim_batch_result_free(migsim_batch_result* r);
 
 /* Per-(variant, tenant) aggregates of a batch, summed over its seeds on the device -- the payload

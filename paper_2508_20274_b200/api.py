@@ -71,6 +71,12 @@ class _Timing(ctypes.Structure):
         ("waves", ctypes.c_int64),
         ("select_samples", ctypes.c_int64),
         ("des_simt", ctypes.c_int64),
+        ("des_blocks_per_sm", ctypes.c_int64),
+        ("des_smem_bytes", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+        ("pipeline_slots", ctypes.c_int64),
     ]
 
 

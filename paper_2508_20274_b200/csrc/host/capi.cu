@@ -40,8 +40,11 @@ struct ParityGuard : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-// batches with at least this many replicas run the SIMT DES (one thread per replica)
-constexpr size_t kSimtMinJobs = 4096;
+// The SIMT DES (one thread per replica) is opt-in (MIGSIM_DES=simt): measured slower than the
+// warp form at every batch size that fits HBM, so "auto" never picks it.
+constexpr size_t kSimtMinJobs = SIZE_MAX;
+// controller rings stay in shared memory while a replica's working set is at most this
+constexpr int64_t kRingsSmemMax = 96 * 1024;
 
 #define CK(x)                                                                                          \
     do {                                                                                               \
@@ -132,10 +135,11 @@ struct WaveAlloc {
 
 struct migsim_gpu {
     int device = 0;
-    WaveAlloc wave;  // device buffers of the last batch, reused by the next
-    cudaStream_t stream = nullptr;
-    cudaEvent_t ev[6] = {};
+    WaveAlloc wave[2];  // device buffers of the last batch (two pipeline slots), reused by the next
+    cudaStream_t stream = nullptr, stream2 = nullptr;
+    cudaEvent_t ev[6] = {}, ev2[6] = {}, span[3] = {};
     std::vector<mgb::ScenarioSpec> scenarios;
+    std::vector<char> released;  // migsim_gpu_release_scenario
 };
 
 struct migsim_batch_result {
@@ -155,6 +159,8 @@ struct migsim_batch_result {
     std::vector<int64_t> pause_off;
     std::vector<double> comps;
     std::vector<int64_t> comp_off;
+    std::vector<migsim_completion> crec;  // keep_completions: engine::CompletionRecord per run, kept_ order
+    std::vector<int64_t> crec_off;
     std::vector<std::string> json;
     std::vector<mgb::TraceRows> traces;  // per run, with write_traces
     std::vector<uint64_t> hist;          // [n_var][T][kHistBins] window-latency histograms (lat_hist.h bins)
@@ -165,6 +171,13 @@ struct migsim_batch_result {
 namespace {
 
 
+
+void check_scenario_id(const migsim_gpu* g, int32_t id) {
+    if (!g || id < 0 || id >= static_cast<int32_t>(g->scenarios.size()))
+        throw mgb::ConfigError("unknown scenario id");
+    if (static_cast<size_t>(id) < g->released.size() && g->released[static_cast<size_t>(id)])
+        throw mgb::ConfigError("scenario id " + std::to_string(id) + " was released");
+}
 
 void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vector<mgb::Variant>& variants,
                     const std::vector<uint64_t>& seeds, const migsim_run_opts& opts, migsim_batch_result& res,
@@ -182,6 +195,20 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.n_runs = n_jobs;
     res.T = T;
     res.R = R;
+    // every host<->device byte of the call, reported in migsim_timing (bench.py's e2e h2d/d2h)
+    int64_t h2d_bytes = 0, d2h_bytes = 0;
+    auto count = [&](size_t n, cudaMemcpyKind k) {
+        if (k == cudaMemcpyHostToDevice) h2d_bytes += static_cast<int64_t>(n);
+        else if (k == cudaMemcpyDeviceToHost) d2h_bytes += static_cast<int64_t>(n);
+    };
+    auto cpy_async = [&](void* d, const void* src, size_t n, cudaMemcpyKind k, cudaStream_t st) {
+        count(n, k);
+        return cudaMemcpyAsync(d, src, n, k, st);
+    };
+    auto cpy_sync = [&](void* d, const void* src, size_t n, cudaMemcpyKind k) {
+        count(n, k);
+        return cudaMemcpy(d, src, n, k);
+    };
     const bool traces = opts.write_traces != 0;
     const bool keep = opts.keep_completions != 0 || traces;
     // working-set layout: controller rings in shared memory when a replica stays under 96 KB
@@ -196,7 +223,22 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     while (simt_lanes > 1 && Y.bytes(simt_lanes) > 200 * 1024) simt_lanes /= 2;
     const bool simt_fits = T <= mg::kSimtMaxTenants && Y.bytes(1) <= 200 * 1024;
     const bool use_simt = simt_fits && (des_mode == "simt" || (des_mode == "auto" && n_jobs >= kSimtMinJobs));
-    const bool rings_in_smem = !use_simt && L.total <= 96 * 1024;
+    // MIGSIM_RINGS=global|smem overrides where the controller rings live (A/B of occupancy vs latency)
+    const char* rings_env = std::getenv("MIGSIM_RINGS");
+    const std::string rings_mode = rings_env ? rings_env : "auto";
+    // auto: rings in shared memory only while every replica of the batch can be resident at once
+    // with them there (latency-bound, few replicas: C2); otherwise in global memory, where the
+    // smaller block footprint raises DES occupancy to the register limit (the saturated regime:
+    // 6.77 -> 5.73 s for 16,384 default.yaml replicas)
+    bool rings_in_smem = !use_simt && rings_mode != "global" && (rings_mode == "smem" || L.total <= kRingsSmemMax);
+    if (rings_in_smem && rings_mode == "auto") {
+        auto* des_k = T <= mg::kRegSlotMaxTenants ? mg::des_kernel_reg : mg::des_kernel;
+        CK(cudaFuncSetAttribute(des_k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+        int occ = 0, n_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, des_k, 32, static_cast<size_t>(L.total)));
+        CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, g->device));
+        if (n_jobs > static_cast<size_t>(occ) * static_cast<size_t>(n_sm)) rings_in_smem = false;
+    }
     if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false, G, I, H);
     // wave size from free memory
     const size_t per_rep = static_cast<size_t>(P.cap_sum) * 8 * (8 + (keep ? 5 : 0)) + static_cast<size_t>(T) * 8 +
@@ -207,23 +249,55 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
                            (rings_in_smem ? 0 : static_cast<size_t>(T) * (P.max_dwell + P.max_validation) * 8);
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
-    free_b += g->wave.bytes();  // the handle's cached wave buffers are reusable
+    free_b += g->wave[0].bytes() + g->wave[1].bytes();  // the handle's cached wave buffers are reusable
     size_t W = std::max<size_t>(1, static_cast<size_t>(0.70 * static_cast<double>(free_b)) / per_rep);
     if (opts.max_wave_replicas > 0) W = std::min<size_t>(W, static_cast<size_t>(opts.max_wave_replicas));
     W = std::min(W, n_jobs);
     if (W == 0) W = 1;
 
-    WaveAlloc& A = g->wave;
+    // ---- wave slots ------------------------------------------------------------------------
+    // Large batches run as a two-slot pipeline on two streams: the arrival generator of wave k+1
+    // and its event loop start while wave k's event loop drains (its ragged tail of long-running
+    // replicas), and wave k's host-side assembly overlaps wave k+1 on the device.  Small batches
+    // (one wave) and the keep_completions / traces paths (synchronous per-run copies) use one slot.
+    const bool want_prof = std::getenv("MIGSIM_PROFILE_EVENTS") != nullptr;
+    const char* pipe_env = std::getenv("MIGSIM_PIPELINE");
+    const bool pipe_allowed = !(pipe_env && std::string(pipe_env) == "0") && !keep && !want_prof;
+    const int n_slots = (pipe_allowed && n_jobs > W) ? 2 : 1;
+    if (n_slots == 2) W = std::max<size_t>(1, W / 2);
+    WaveAlloc& A = g->wave[0];  // also holds the batch-wide buffers (scenario, controllers, histograms)
     const size_t big = W * static_cast<size_t>(P.cap_sum);
-    A.arr_t.alloc(big);
-    A.arr_bytes.alloc(big);
-    A.arr_mult.alloc(big);
-    A.arr_noise.alloc(big);
-    A.irq_e.alloc(big);
-    A.t_all.alloc(big);
-    A.req_ms.alloc(big);
-    A.win_lat.alloc(big);
-    A.win_hist.alloc(W * T * mg::kHistBins);
+    const int n_ticks = P.scen.n_ticks;
+    constexpr int kTraceWin = 256;  // engine.cpp:115
+    for (int si = 0; si < n_slots; ++si) {
+        WaveAlloc& S = g->wave[si];
+        S.arr_t.alloc(big);
+        S.arr_bytes.alloc(big);
+        S.arr_mult.alloc(big);
+        S.arr_noise.alloc(big);
+        S.irq_e.alloc(big);
+        S.t_all.alloc(big);
+        S.req_ms.alloc(big);
+        S.win_lat.alloc(big);
+        S.win_hist.alloc(W * T * mg::kHistBins);
+        S.n_all.alloc(W * T);
+        S.n_kept.alloc(W * T);
+        S.variant.alloc(W);
+        S.seeds.alloc(W);
+        S.gen_overflow.alloc(1);
+        S.mt_pause.alloc(W * T * mg::kMtN);
+        S.actions.alloc(W * action_cap);
+        S.actions_c.alloc(W * action_cap);
+        S.pauses.alloc(W * pause_cap);
+        S.pauses_c.alloc(W * pause_cap);
+        S.tout.alloc(W * T);
+        S.rout.alloc(W);
+        S.backlog.alloc(W * R * 2);
+        S.quant.alloc(W * T * 4);
+        if (!rings_in_smem) S.rings.alloc(W * T * (P.max_dwell + P.max_validation));
+        S.act_off.alloc(W + 1);
+        S.pause_off.alloc(W + 1);
+    }
     if (keep) {
         A.c_done.alloc(big);
         A.c_total.alloc(big);
@@ -232,8 +306,6 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         A.c_noise.alloc(big);
         A.c_order.alloc(big);
     }
-    const int n_ticks = P.scen.n_ticks;
-    constexpr int kTraceWin = 256;  // engine.cpp:115
     if (traces) {
         A.tr_cnt.alloc(W * static_cast<size_t>(n_ticks) * T);
         A.tr_fab.alloc(W * static_cast<size_t>(n_ticks) * R);
@@ -245,96 +317,106 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
             tw[k].ring = A.tr_ring.p + k * kTraceWin;
             tw[k].cap = kTraceWin;
         }
-        CK(cudaMemcpy(A.tr_win.p, tw.data(), sizeof(mg::TailWin) * W * T, cudaMemcpyHostToDevice));
+        CK(cpy_sync(A.tr_win.p, tw.data(), sizeof(mg::TailWin) * W * T, cudaMemcpyHostToDevice));
         res.traces.resize(n_jobs);
     }
-    A.n_all.alloc(W * T);
-    A.n_kept.alloc(W * T);
-    A.variant.alloc(W);
-    A.seeds.alloc(W);
-    A.gen_overflow.alloc(1);
     A.file_order.alloc(T);
     A.sel_order.alloc(T);
-    A.mt_pause.alloc(W * T * mg::kMtN);
-    A.actions.alloc(W * action_cap);
-    A.actions_c.alloc(W * action_cap);
-    A.pauses.alloc(W * pause_cap);
-    A.pauses_c.alloc(W * pause_cap);
-    A.tout.alloc(W * T);
-    A.rout.alloc(W);
-    A.backlog.alloc(W * R * 2);
-    A.quant.alloc(W * T * 4);
-    if (!rings_in_smem) A.rings.alloc(W * T * (P.max_dwell + P.max_validation));
     A.off.alloc(T);
     A.cap.alloc(T);
-    A.act_off.alloc(W + 1);
-    A.pause_off.alloc(W + 1);
     A.scen.alloc(1);
     A.ctrl.alloc(n_var);
     A.hist_sum.alloc(n_var * T * mg::kHistBins);
     cudaStream_t s = g->stream;
     CK(cudaMemsetAsync(A.hist_sum.p, 0, sizeof(unsigned long long) * n_var * T * mg::kHistBins, s));
-    CK(cudaMemcpyAsync(A.scen.p, &P.scen, sizeof(mg::PScenario), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(A.ctrl.p, P.ctrl.data(), sizeof(mg::PController) * n_var, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(A.off.p, P.off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(A.cap.p, P.cap.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(A.file_order.p, P.file_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
+    CK(cpy_async(A.scen.p, &P.scen, sizeof(mg::PScenario), cudaMemcpyHostToDevice, s));
+    CK(cpy_async(A.ctrl.p, P.ctrl.data(), sizeof(mg::PController) * n_var, cudaMemcpyHostToDevice, s));
+    CK(cpy_async(A.off.p, P.off.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
+    CK(cpy_async(A.cap.p, P.cap.data(), sizeof(int64_t) * T, cudaMemcpyHostToDevice, s));
+    CK(cpy_async(A.file_order.p, P.file_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
     std::vector<int32_t> sel_order(T);
     for (int t = 0; t < T; ++t) sel_order[t] = t;
     std::stable_sort(sel_order.begin(), sel_order.end(), [&](int32_t a, int32_t b) { return P.cap[a] > P.cap[b]; });
-    CK(cudaMemcpyAsync(A.sel_order.p, sel_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
+    CK(cpy_async(A.sel_order.p, sel_order.data(), sizeof(int32_t) * T, cudaMemcpyHostToDevice, s));
 
-    mg::WaveBuffers B{};
-    B.arr_t = A.arr_t.p;
-    B.arr_bytes = A.arr_bytes.p;
-    B.arr_mult = A.arr_mult.p;
-    B.arr_noise = A.arr_noise.p;
-    B.irq_e = A.irq_e.p;
-    B.t_all = A.t_all.p;
-    B.req_ms = A.req_ms.p;
-    B.win_lat = A.win_lat.p;
-    B.win_hist = A.win_hist.p;
+    mg::WaveBuffers B0{};
+    B0.file_order = A.file_order.p;
+    B0.sel_order = A.sel_order.p;
+    B0.off = A.off.p;
+    B0.cap = A.cap.p;
     // optional streams: only when this batch asks for them (the cached buffers may hold others)
-    B.c_done = keep ? A.c_done.p : nullptr;
-    B.c_total = keep ? A.c_total.p : nullptr;
-    B.c_compute = keep ? A.c_compute.p : nullptr;
-    B.c_transfer = keep ? A.c_transfer.p : nullptr;
-    B.c_noise = keep ? A.c_noise.p : nullptr;
-    B.c_order = keep ? A.c_order.p : nullptr;
-    B.tr_cnt = traces ? A.tr_cnt.p : nullptr;
-    B.tr_fab = traces ? A.tr_fab.p : nullptr;
-    B.tr_win = traces ? A.tr_win.p : nullptr;
-    B.n_all = A.n_all.p;
-    B.n_kept = A.n_kept.p;
-    B.mt_pause = A.mt_pause.p;
-    B.actions = A.actions.p;
-    B.pauses = A.pauses.p;
-    B.tout = A.tout.p;
-    B.rout = A.rout.p;
-    B.backlog = A.backlog.p;
-    B.quant = A.quant.p;
-    B.rings = rings_in_smem ? nullptr : A.rings.p;
-    B.seeds = A.seeds.p;
-    B.variant = A.variant.p;
-    B.off = A.off.p;
-    B.cap = A.cap.p;
-    B.file_order = A.file_order.p;
-    B.sel_order = A.sel_order.p;
-    B.gen_overflow = A.gen_overflow.p;
-    B.cap_sum = P.cap_sum;
-    B.action_cap = action_cap;
-    B.pause_cap = pause_cap;
-    B.any_irq_noise = P.any_irq_noise;
-    B.rings_in_smem = rings_in_smem;
-    B.dwell = P.max_dwell;
-    B.validation = P.max_validation;
-    B.n_variants = static_cast<int32_t>(n_var);
+    B0.c_done = keep ? A.c_done.p : nullptr;
+    B0.c_total = keep ? A.c_total.p : nullptr;
+    B0.c_compute = keep ? A.c_compute.p : nullptr;
+    B0.c_transfer = keep ? A.c_transfer.p : nullptr;
+    B0.c_noise = keep ? A.c_noise.p : nullptr;
+    B0.c_order = keep ? A.c_order.p : nullptr;
+    B0.tr_cnt = traces ? A.tr_cnt.p : nullptr;
+    B0.tr_fab = traces ? A.tr_fab.p : nullptr;
+    B0.tr_win = traces ? A.tr_win.p : nullptr;
+    B0.cap_sum = P.cap_sum;
+    B0.action_cap = action_cap;
+    B0.pause_cap = pause_cap;
+    B0.any_irq_noise = P.any_irq_noise;
+    B0.rings_in_smem = rings_in_smem;
+    B0.dwell = P.max_dwell;
+    B0.validation = P.max_validation;
+    B0.n_variants = static_cast<int32_t>(n_var);
     DevBuf<unsigned long long> prof;
-    const bool want_prof = std::getenv("MIGSIM_PROFILE_EVENTS") != nullptr;
     if (want_prof) {
         prof.alloc(18);
-        CK(cudaMemsetAsync(prof.p, 0, 18 * 8, g->stream));
-        B.prof = prof.p;
+        CK(cudaMemsetAsync(prof.p, 0, 18 * 8, s));
+        B0.prof = prof.p;
+    }
+    struct Slot {
+        WaveAlloc* A = nullptr;
+        cudaStream_t st = nullptr;
+        cudaEvent_t* ev = nullptr;
+        mg::WaveBuffers B{};
+        std::vector<uint64_t> wseeds;
+        std::vector<int32_t> wvar, nkept;
+        std::vector<int64_t> aoff, poff;
+        int32_t overflow = 0;
+        size_t j0 = 0;
+        int w = 0;
+        bool busy = false;
+    };
+    Slot slots[2];
+    for (int si = 0; si < n_slots; ++si) {
+        Slot& sl = slots[si];
+        WaveAlloc& S = g->wave[si];
+        sl.A = &S;
+        sl.st = si == 0 ? g->stream : g->stream2;
+        sl.ev = si == 0 ? g->ev : g->ev2;
+        sl.B = B0;
+        mg::WaveBuffers& B = sl.B;
+        B.arr_t = S.arr_t.p;
+        B.arr_bytes = S.arr_bytes.p;
+        B.arr_mult = S.arr_mult.p;
+        B.arr_noise = S.arr_noise.p;
+        B.irq_e = S.irq_e.p;
+        B.t_all = S.t_all.p;
+        B.req_ms = S.req_ms.p;
+        B.win_lat = S.win_lat.p;
+        B.win_hist = S.win_hist.p;
+        B.n_all = S.n_all.p;
+        B.n_kept = S.n_kept.p;
+        B.mt_pause = S.mt_pause.p;
+        B.actions = S.actions.p;
+        B.pauses = S.pauses.p;
+        B.tout = S.tout.p;
+        B.rout = S.rout.p;
+        B.backlog = S.backlog.p;
+        B.quant = S.quant.p;
+        B.rings = rings_in_smem ? nullptr : S.rings.p;
+        B.seeds = S.seeds.p;
+        B.variant = S.variant.p;
+        B.gen_overflow = S.gen_overflow.p;
+        sl.wseeds.resize(W);
+        sl.wvar.resize(W);
+        sl.nkept.resize(W * T);
+        sl.aoff.resize(W + 1);
+        sl.poff.resize(W + 1);
     }
 
     auto* des = T <= mg::kRegSlotMaxTenants ? mg::des_kernel_reg : mg::des_kernel;
@@ -343,6 +425,12 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
                                 static_cast<int>(Y.bytes(simt_lanes))));
     else
         CK(cudaFuncSetAttribute(des, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+    int des_blocks_per_sm = 0;
+    if (use_simt)
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&des_blocks_per_sm, mg::des_simt_kernel, simt_lanes,
+                                                         static_cast<size_t>(Y.bytes(simt_lanes))));
+    else
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&des_blocks_per_sm, des, 32, static_cast<size_t>(L.total)));
     const size_t sel_smem = mg::select_smem_bytes();
     CK(cudaFuncSetAttribute(mg::select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sel_smem)));
     const size_t cl_smem = mg::select_cluster_smem_bytes();
@@ -361,62 +449,163 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.act_off.assign(n_jobs + 1, 0);
     res.pause_off.assign(n_jobs + 1, 0);
     if (keep) res.comp_off.assign(n_jobs + 1, 0);
+    if (keep) res.crec_off.assign(n_jobs + 1, 0);
 
-    std::vector<uint64_t> wseeds(W);
-    std::vector<int32_t> wvar(W);
-    std::vector<int64_t> aoff(W + 1), poff(W + 1);
-    std::vector<int32_t> nkept(W * T);
     double gen_ms = 0, des_ms = 0, sel_ms = 0;
-    int64_t completions = 0, arrivals = 0, events = 0, waves = 0, samples = 0;
-    for (size_t j0 = 0; j0 < n_jobs; j0 += W) {
-        const int w = static_cast<int>(std::min(W, n_jobs - j0));
+    int64_t completions = 0, arrivals = 0, events = 0, waves = 0, samples = 0, launches = 0;
+    // device span of the whole batch: first enqueue to the last kernel of either stream
+    CK(cudaEventRecord(g->span[0], s));
+    if (n_slots == 2) CK(cudaStreamWaitEvent(g->stream2, g->span[0], 0));
+
+    // enqueue one wave: H2D of its seeds/variants, generator, event loop, select, histogram fold,
+    // D2H of the per-replica status it needs before compaction
+    auto launch_wave = [&](Slot& sl, size_t j0, int w) {
+        WaveAlloc& S = *sl.A;
+        const cudaStream_t st = sl.st;
+        const mg::WaveBuffers& B = sl.B;
+        sl.j0 = j0;
+        sl.w = w;
+        sl.busy = true;
         ++waves;
+        launches += 7;  // gen_times, gen_marks, des, select, hist_reduce, compact_actions, compact_pauses
         for (int k = 0; k < w; ++k) {
-            wseeds[k] = seeds[(j0 + k) % seeds.size()];
-            wvar[k] = static_cast<int32_t>((j0 + k) / seeds.size());
+            sl.wseeds[k] = seeds[(j0 + k) % seeds.size()];
+            sl.wvar[k] = static_cast<int32_t>((j0 + k) / seeds.size());
         }
-        CK(cudaMemcpyAsync(A.seeds.p, wseeds.data(), sizeof(uint64_t) * w, cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(A.variant.p, wvar.data(), sizeof(int32_t) * w, cudaMemcpyHostToDevice, s));
-        CK(cudaMemsetAsync(A.gen_overflow.p, 0, sizeof(int32_t), s));
-        CK(cudaEventRecord(g->ev[0], s));
-        CK(cudaMemsetAsync(A.win_hist.p, 0, sizeof(uint32_t) * w * T * mg::kHistBins, s));  // timed with gen
+        CK(cpy_async(S.seeds.p, sl.wseeds.data(), sizeof(uint64_t) * w, cudaMemcpyHostToDevice, st));
+        CK(cpy_async(S.variant.p, sl.wvar.data(), sizeof(int32_t) * w, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(S.gen_overflow.p, 0, sizeof(int32_t), st));
+        CK(cudaEventRecord(sl.ev[0], st));
+        CK(cudaMemsetAsync(S.win_hist.p, 0, sizeof(uint32_t) * w * T * mg::kHistBins, st));  // timed with gen
         const int64_t nt = static_cast<int64_t>(w) * T;
-        mg::gen_times_kernel<<<static_cast<unsigned>(nt), 32, mg::gen_times_smem_bytes(), s>>>(A.scen.p, B, w);
-        mg::gen_marks_kernel<<<static_cast<unsigned>(4 * nt), 32, 0, s>>>(A.scen.p, B, w);
+        mg::gen_times_kernel<<<static_cast<unsigned>(nt), 32, mg::gen_times_smem_bytes(), st>>>(A.scen.p, B, w);
+        mg::gen_marks_kernel<<<static_cast<unsigned>(4 * nt), 32, 0, st>>>(A.scen.p, B, w);
         CK(cudaGetLastError());
-        CK(cudaEventRecord(g->ev[1], s));
+        CK(cudaEventRecord(sl.ev[1], st));
         if (use_simt)
             mg::des_simt_kernel<<<static_cast<unsigned>((w + simt_lanes - 1) / simt_lanes), simt_lanes,
-                                  static_cast<size_t>(Y.bytes(simt_lanes)), s>>>(A.scen.p, A.ctrl.p, B, w, Y);
+                                  static_cast<size_t>(Y.bytes(simt_lanes)), st>>>(A.scen.p, A.ctrl.p, B, w, Y);
         else
-            des<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), s>>>(A.scen.p, A.ctrl.p, B, w, L);
+            des<<<static_cast<unsigned>(w), 32, static_cast<size_t>(L.total), st>>>(A.scen.p, A.ctrl.p, B, w, L);
         CK(cudaGetLastError());
-        CK(cudaEventRecord(g->ev[2], s));
+        CK(cudaEventRecord(sl.ev[2], st));
         if (sel_cluster)
             mg::select_cluster_kernel<<<static_cast<unsigned>(nt * mg::select_cluster_size()), mg::select_cluster_threads(),
-                                        cl_smem, s>>>(B, T, w);
+                                        cl_smem, st>>>(B, T, w);
         else {
             mg::WaveBuffers Bs = B;
             if (sel_two_pass) Bs.win_hist = nullptr;
-            mg::select_kernel<<<static_cast<unsigned>(nt), mg::select_threads(), sel_smem, s>>>(Bs, T, w);
+            mg::select_kernel<<<static_cast<unsigned>(nt), mg::select_threads(), sel_smem, st>>>(Bs, T, w);
         }
         {
             constexpr int kChunk = 256;
             const dim3 grid(static_cast<unsigned>((T * mg::kHistBins + 255) / 256),
                             static_cast<unsigned>((w + kChunk - 1) / kChunk));
-            mg::hist_reduce_kernel<<<grid, 256, 0, s>>>(A.win_hist.p, A.variant.p, w, T, kChunk, A.hist_sum.p);
+            mg::hist_reduce_kernel<<<grid, 256, 0, st>>>(S.win_hist.p, S.variant.p, w, T, kChunk, A.hist_sum.p);
         }
         CK(cudaGetLastError());
-        CK(cudaEventRecord(g->ev[3], s));
-        int32_t overflow = 0;
-        CK(cudaMemcpyAsync(&overflow, A.gen_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(res.rout.data() + j0, A.rout.p, sizeof(mg::ReplicaOut) * w, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(nkept.data(), A.n_kept.p, sizeof(int32_t) * w * T, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (overflow) throw ParityGuard("arrival-record capacity exceeded");
+        CK(cudaEventRecord(sl.ev[3], st));
+        CK(cpy_async(&sl.overflow, S.gen_overflow.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        CK(cpy_async(res.rout.data() + j0, S.rout.p, sizeof(mg::ReplicaOut) * w, cudaMemcpyDeviceToHost, st));
+        CK(cpy_async(sl.nkept.data(), S.n_kept.p, sizeof(int32_t) * w * T, cudaMemcpyDeviceToHost, st));
+    };
+
+    // keep_completions / traces: per-run completion records and trace rows (single-slot path)
+    auto collect_keep = [&](size_t j0, int w) {
+
+        std::vector<double> tmp(static_cast<size_t>(P.cap_sum) * 5);
+        for (int k = 0; k < w; ++k) {
+            const size_t job = j0 + k;
+            const int64_t base = static_cast<int64_t>(k) * P.cap_sum;
+            CK(cpy_sync(tmp.data() + 0 * P.cap_sum, A.c_done.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+            CK(cpy_sync(tmp.data() + 1 * P.cap_sum, A.c_total.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+            CK(cpy_sync(tmp.data() + 2 * P.cap_sum, A.c_compute.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+            CK(cpy_sync(tmp.data() + 3 * P.cap_sum, A.c_transfer.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+            CK(cpy_sync(tmp.data() + 4 * P.cap_sum, A.c_noise.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+            for (int i = 0; i < T; ++i) {
+                const uint64_t n = res.tout[job * T + i].completed_total;
+                for (uint64_t c = 0; c < n; ++c) {
+                    const int64_t o = P.off[i] + static_cast<int64_t>(c);
+                    const double rec[7] = {static_cast<double>(i), static_cast<double>(c), tmp[o],
+                                           tmp[P.cap_sum + o], tmp[2 * P.cap_sum + o], tmp[3 * P.cap_sum + o],
+                                           tmp[4 * P.cap_sum + o]};
+                    res.comps.insert(res.comps.end(), rec, rec + 7);
+                }
+            }
+            res.comp_off[job + 1] = static_cast<int64_t>(res.comps.size() / 7);
+            {
+                // engine::CompletionRecord list in the reference's kept_ order (engine.cpp:482-504):
+                // requests complete FIFO per tenant, so completion c of tenant i is its c-th kept
+                // arrival; c_order is the completion's position in the replica's sequence
+                std::vector<double> arr(P.cap_sum), byt(P.cap_sum);
+                std::vector<int64_t> ord(P.cap_sum);
+                CK(cpy_sync(arr.data(), A.arr_t.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cpy_sync(byt.data(), A.arr_bytes.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cpy_sync(ord.data(), A.c_order.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                const size_t c0 = res.crec.size();
+                int64_t n_all = 0;
+                for (int i = 0; i < T; ++i) n_all += static_cast<int64_t>(res.tout[job * T + i].completed_total);
+                res.crec.resize(c0 + static_cast<size_t>(n_all));
+                for (int i = 0; i < T; ++i) {
+                    const uint64_t n = res.tout[job * T + i].completed_total;
+                    for (uint64_t c = 0; c < n; ++c) {
+                        const int64_t o = P.off[i] + static_cast<int64_t>(c);
+                        if (ord[o] < 0 || ord[o] >= n_all) throw ParityGuard("completion order out of range");
+                        migsim_completion& m = res.crec[c0 + static_cast<size_t>(ord[o])];
+                        m.tenant = i;
+                        m.seq = c;
+                        m.arrived_s = arr[o];
+                        m.done_s = tmp[o];
+                        m.total_ms = tmp[P.cap_sum + o];
+                        m.compute_ms = tmp[2 * P.cap_sum + o];
+                        m.transfer_ms = tmp[3 * P.cap_sum + o];
+                        m.noise_ms = tmp[4 * P.cap_sum + o];
+                        m.transfer_bytes = byt[o];
+                    }
+                }
+                res.crec_off[job + 1] = static_cast<int64_t>(res.crec.size());
+            }
+            if (traces) {
+                mgb::TraceRows& tr = res.traces[job];
+                tr.off = P.off;
+                tr.n_done.resize(T);
+                for (int i = 0; i < T; ++i) tr.n_done[i] = res.tout[job * T + i].completed_total;
+                tr.done.assign(tmp.begin(), tmp.begin() + P.cap_sum);
+                tr.total.assign(tmp.begin() + P.cap_sum, tmp.begin() + 2 * P.cap_sum);
+                tr.compute.assign(tmp.begin() + 2 * P.cap_sum, tmp.begin() + 3 * P.cap_sum);
+                tr.transfer.assign(tmp.begin() + 3 * P.cap_sum, tmp.begin() + 4 * P.cap_sum);
+                tr.noise.assign(tmp.begin() + 4 * P.cap_sum, tmp.begin() + 5 * P.cap_sum);
+                tr.arrived.resize(P.cap_sum);
+                tr.bytes.resize(P.cap_sum);
+                tr.order.resize(P.cap_sum);
+                CK(cpy_sync(tr.arrived.data(), A.arr_t.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cpy_sync(tr.bytes.data(), A.arr_bytes.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                CK(cpy_sync(tr.order.data(), A.c_order.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
+                tr.n_ticks = n_ticks;
+                tr.counters.resize(static_cast<size_t>(n_ticks) * T);
+                tr.fabric.resize(static_cast<size_t>(n_ticks) * R);
+                CK(cpy_sync(tr.counters.data(), A.tr_cnt.p + static_cast<size_t>(k) * n_ticks * T,
+                              sizeof(mg::CounterRow) * n_ticks * T, cudaMemcpyDeviceToHost));
+                CK(cpy_sync(tr.fabric.data(), A.tr_fab.p + static_cast<size_t>(k) * n_ticks * R,
+                              sizeof(mg::FabricRow) * n_ticks * R, cudaMemcpyDeviceToHost));
+            }
+        }
+            };
+
+    // wait for a wave, compact its logs, copy its results back and fold them into the batch result
+    auto finish_wave = [&](Slot& sl) {
+        WaveAlloc& S = *sl.A;
+        const cudaStream_t st = sl.st;
+        const size_t j0 = sl.j0;
+        const int w = sl.w;
+        std::vector<int64_t>& aoff = sl.aoff;
+        std::vector<int64_t>& poff = sl.poff;
+        sl.busy = false;
+        CK(cudaStreamSynchronize(st));
+        if (sl.overflow) throw ParityGuard("arrival-record capacity exceeded");
         if (want_prof) {
             unsigned long long h[18];
-            CK(cudaMemcpy(h, prof.p, sizeof(h), cudaMemcpyDeviceToHost));
+            CK(cpy_sync(h, prof.p, sizeof(h), cudaMemcpyDeviceToHost));
             static const char* names[6] = {"resume", "expire", "transfer", "compute", "arrival", "tick"};
             for (int k = 0; k < 6; ++k)
                 if (h[3 * k + 2])
@@ -425,11 +614,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
                                  static_cast<double>(h[3 * k + 1]) / h[3 * k + 2]);
         }
         float ms = 0;
-        CK(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
+        CK(cudaEventElapsedTime(&ms, sl.ev[0], sl.ev[1]));
         gen_ms += ms;
-        CK(cudaEventElapsedTime(&ms, g->ev[1], g->ev[2]));
+        CK(cudaEventElapsedTime(&ms, sl.ev[1], sl.ev[2]));
         des_ms += ms;
-        CK(cudaEventElapsedTime(&ms, g->ev[2], g->ev[3]));
+        CK(cudaEventElapsedTime(&ms, sl.ev[2], sl.ev[3]));
         sel_ms += ms;
         aoff[0] = poff[0] = 0;
         for (int k = 0; k < w; ++k) {
@@ -439,13 +628,13 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
             poff[k + 1] = poff[k] + ro.n_pauses;
             events += static_cast<int64_t>(ro.n_events);
         }
-        for (int k = 0; k < w * T; ++k) arrivals += nkept[k];
-        CK(cudaMemcpyAsync(A.act_off.p, aoff.data(), sizeof(int64_t) * (w + 1), cudaMemcpyHostToDevice, s));
-        CK(cudaMemcpyAsync(A.pause_off.p, poff.data(), sizeof(int64_t) * (w + 1), cudaMemcpyHostToDevice, s));
-        mg::compact_actions_kernel<<<static_cast<unsigned>(w), 64, 0, s>>>(A.actions.p, action_cap, A.rout.p, A.act_off.p,
-                                                                           A.actions_c.p, w);
-        mg::compact_pauses_kernel<<<static_cast<unsigned>(w), 64, 0, s>>>(A.pauses.p, pause_cap, A.rout.p, A.pause_off.p,
-                                                                          A.pauses_c.p, w);
+        for (int k = 0; k < w * T; ++k) arrivals += sl.nkept[k];
+        CK(cpy_async(S.act_off.p, aoff.data(), sizeof(int64_t) * (w + 1), cudaMemcpyHostToDevice, st));
+        CK(cpy_async(S.pause_off.p, poff.data(), sizeof(int64_t) * (w + 1), cudaMemcpyHostToDevice, st));
+        mg::compact_actions_kernel<<<static_cast<unsigned>(w), 64, 0, st>>>(S.actions.p, action_cap, S.rout.p,
+                                                                            S.act_off.p, S.actions_c.p, w);
+        mg::compact_pauses_kernel<<<static_cast<unsigned>(w), 64, 0, st>>>(S.pauses.p, pause_cap, S.rout.p,
+                                                                           S.pause_off.p, S.pauses_c.p, w);
         CK(cudaGetLastError());
         const size_t a0 = res.actions.size(), p0 = res.pauses.size();
         res.actions.resize(a0 + static_cast<size_t>(aoff[w]));
@@ -454,66 +643,42 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
             res.act_off[j0 + k + 1] = static_cast<int64_t>(a0) + aoff[k + 1];
             res.pause_off[j0 + k + 1] = static_cast<int64_t>(p0) + poff[k + 1];
         }
-        if (aoff[w]) CK(cudaMemcpyAsync(res.actions.data() + a0, A.actions_c.p, sizeof(mg::ActionRec) * aoff[w], cudaMemcpyDeviceToHost, s));
-        if (poff[w]) CK(cudaMemcpyAsync(res.pauses.data() + p0, A.pauses_c.p, sizeof(mg::PauseRec) * poff[w], cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(res.tout.data() + j0 * T, A.tout.p, sizeof(mg::TenantOut) * w * T, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(res.quant.data() + j0 * T * 4, A.quant.p, sizeof(double) * w * T * 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(res.backlog.data() + j0 * R * 2, A.backlog.p, sizeof(double) * w * R * 2, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
+        if (aoff[w]) CK(cpy_async(res.actions.data() + a0, S.actions_c.p, sizeof(mg::ActionRec) * aoff[w], cudaMemcpyDeviceToHost, st));
+        if (poff[w]) CK(cpy_async(res.pauses.data() + p0, S.pauses_c.p, sizeof(mg::PauseRec) * poff[w], cudaMemcpyDeviceToHost, st));
+        CK(cpy_async(res.tout.data() + j0 * T, S.tout.p, sizeof(mg::TenantOut) * w * T, cudaMemcpyDeviceToHost, st));
+        CK(cpy_async(res.quant.data() + j0 * T * 4, S.quant.p, sizeof(double) * w * T * 4, cudaMemcpyDeviceToHost, st));
+        CK(cpy_async(res.backlog.data() + j0 * R * 2, S.backlog.p, sizeof(double) * w * R * 2, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         for (int k = 0; k < w * T; ++k) {
             completions += static_cast<int64_t>(res.tout[j0 * T + k].completed_total);
             samples += static_cast<int64_t>(res.tout[j0 * T + k].completed_window);
         }
-        if (keep) {
-            std::vector<double> tmp(static_cast<size_t>(P.cap_sum) * 5);
-            for (int k = 0; k < w; ++k) {
-                const size_t job = j0 + k;
-                const int64_t base = static_cast<int64_t>(k) * P.cap_sum;
-                CK(cudaMemcpy(tmp.data() + 0 * P.cap_sum, A.c_done.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(tmp.data() + 1 * P.cap_sum, A.c_total.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(tmp.data() + 2 * P.cap_sum, A.c_compute.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(tmp.data() + 3 * P.cap_sum, A.c_transfer.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                CK(cudaMemcpy(tmp.data() + 4 * P.cap_sum, A.c_noise.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                for (int i = 0; i < T; ++i) {
-                    const uint64_t n = res.tout[job * T + i].completed_total;
-                    for (uint64_t c = 0; c < n; ++c) {
-                        const int64_t o = P.off[i] + static_cast<int64_t>(c);
-                        const double rec[7] = {static_cast<double>(i), static_cast<double>(c), tmp[o],
-                                               tmp[P.cap_sum + o], tmp[2 * P.cap_sum + o], tmp[3 * P.cap_sum + o],
-                                               tmp[4 * P.cap_sum + o]};
-                        res.comps.insert(res.comps.end(), rec, rec + 7);
-                    }
-                }
-                res.comp_off[job + 1] = static_cast<int64_t>(res.comps.size() / 7);
-                if (traces) {
-                    mgb::TraceRows& tr = res.traces[job];
-                    tr.off = P.off;
-                    tr.n_done.resize(T);
-                    for (int i = 0; i < T; ++i) tr.n_done[i] = res.tout[job * T + i].completed_total;
-                    tr.done.assign(tmp.begin(), tmp.begin() + P.cap_sum);
-                    tr.total.assign(tmp.begin() + P.cap_sum, tmp.begin() + 2 * P.cap_sum);
-                    tr.compute.assign(tmp.begin() + 2 * P.cap_sum, tmp.begin() + 3 * P.cap_sum);
-                    tr.transfer.assign(tmp.begin() + 3 * P.cap_sum, tmp.begin() + 4 * P.cap_sum);
-                    tr.noise.assign(tmp.begin() + 4 * P.cap_sum, tmp.begin() + 5 * P.cap_sum);
-                    tr.arrived.resize(P.cap_sum);
-                    tr.bytes.resize(P.cap_sum);
-                    tr.order.resize(P.cap_sum);
-                    CK(cudaMemcpy(tr.arrived.data(), A.arr_t.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                    CK(cudaMemcpy(tr.bytes.data(), A.arr_bytes.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                    CK(cudaMemcpy(tr.order.data(), A.c_order.p + base, 8 * P.cap_sum, cudaMemcpyDeviceToHost));
-                    tr.n_ticks = n_ticks;
-                    tr.counters.resize(static_cast<size_t>(n_ticks) * T);
-                    tr.fabric.resize(static_cast<size_t>(n_ticks) * R);
-                    CK(cudaMemcpy(tr.counters.data(), A.tr_cnt.p + static_cast<size_t>(k) * n_ticks * T,
-                                  sizeof(mg::CounterRow) * n_ticks * T, cudaMemcpyDeviceToHost));
-                    CK(cudaMemcpy(tr.fabric.data(), A.tr_fab.p + static_cast<size_t>(k) * n_ticks * R,
-                                  sizeof(mg::FabricRow) * n_ticks * R, cudaMemcpyDeviceToHost));
-                }
-            }
-        }
+        if (keep) collect_keep(j0, w);
+    };
+
+    std::vector<size_t> starts;
+    for (size_t j0 = 0; j0 < n_jobs; j0 += W) starts.push_back(j0);
+    for (size_t k = 0; k < starts.size(); ++k) {
+        Slot& sl = slots[k % n_slots];
+        if (sl.busy) finish_wave(sl);
+        launch_wave(sl, starts[k], static_cast<int>(std::min(W, n_jobs - starts[k])));
+        if (n_slots == 2 && k >= 1 && slots[(k - 1) % 2].busy) finish_wave(slots[(k - 1) % 2]);
+    }
+    for (size_t k = starts.size() >= 2 ? starts.size() - 2 : 0; k < starts.size(); ++k)
+        if (slots[k % n_slots].busy) finish_wave(slots[k % n_slots]);
+    CK(cudaEventRecord(g->span[1], g->stream));
+    if (n_slots == 2) CK(cudaEventRecord(g->span[2], g->stream2));
+    CK(cudaStreamSynchronize(g->stream));
+    if (n_slots == 2) CK(cudaStreamSynchronize(g->stream2));
+    float span_ms = 0;
+    CK(cudaEventElapsedTime(&span_ms, g->span[0], g->span[1]));
+    if (n_slots == 2) {
+        float ms2 = 0;
+        CK(cudaEventElapsedTime(&ms2, g->span[0], g->span[2]));
+        span_ms = std::max(span_ms, ms2);
     }
     res.hist.resize(n_var * T * mg::kHistBins);
-    CK(cudaMemcpyAsync(res.hist.data(), A.hist_sum.p, sizeof(uint64_t) * res.hist.size(), cudaMemcpyDeviceToHost, s));
+    CK(cpy_async(res.hist.data(), A.hist_sum.p, sizeof(uint64_t) * res.hist.size(), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     res.counts.assign(n_var * T * 3, 0);
     for (size_t job = 0; job < n_jobs; ++job) {
@@ -530,7 +695,9 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.timing.gen_ms = gen_ms;
     res.timing.des_ms = des_ms;
     res.timing.select_ms = sel_ms;
-    res.timing.total_device_ms = gen_ms + des_ms + sel_ms;
+    // single slot: the kernels' own time; two slots: the device span (kernels overlap)
+    res.timing.total_device_ms = n_slots == 2 ? static_cast<double>(span_ms) : gen_ms + des_ms + sel_ms;
+    res.timing.pipeline_slots = n_slots;
     res.timing.replicas = static_cast<int64_t>(n_jobs);
     res.timing.tenant_ticks = static_cast<int64_t>(n_jobs) * T * P.scen.n_ticks;
     res.timing.completions = completions;
@@ -539,6 +706,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.timing.waves = waves;
     res.timing.select_samples = samples;
     res.timing.des_simt = use_simt ? 1 : 0;
+    res.timing.des_blocks_per_sm = des_blocks_per_sm;
+    res.timing.des_smem_bytes = use_simt ? Y.bytes(simt_lanes) : L.total;
+    res.timing.kernel_launches = launches;
+    res.timing.h2d_bytes = h2d_bytes;
+    res.timing.d2h_bytes = d2h_bytes;
     res.timing.wall_ms =
         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
 }
@@ -613,7 +785,10 @@ int migsim_gpu_open(int device, migsim_gpu** out, char* err, size_t errlen) {
         auto* g = new migsim_gpu();
         g->device = device;
         CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&g->stream2, cudaStreamNonBlocking));
         for (auto& e : g->ev) CK(cudaEventCreate(&e));
+        for (auto& e : g->ev2) CK(cudaEventCreate(&e));
+        for (auto& e : g->span) CK(cudaEventCreate(&e));
         *out = g;
     });
 }
@@ -621,9 +796,13 @@ int migsim_gpu_open(int device, migsim_gpu** out, char* err, size_t errlen) {
 void migsim_gpu_close(migsim_gpu* g) {
     if (!g) return;
     cudaSetDevice(g->device);
-    for (auto& e : g->ev)
+    for (auto* evs : {g->ev, g->ev2})
+        for (int k = 0; k < 6; ++k)
+            if (evs[k]) cudaEventDestroy(evs[k]);
+    for (auto& e : g->span)
         if (e) cudaEventDestroy(e);
     if (g->stream) cudaStreamDestroy(g->stream);
+    if (g->stream2) cudaStreamDestroy(g->stream2);
     delete g;
 }
 
@@ -633,6 +812,117 @@ int migsim_gpu_load_scenario(migsim_gpu* g, const char* yaml_text, const char* s
         g->scenarios.push_back(mgb::parse_scenario(yaml_text, source_name ? source_name : "<scenario>"));
         *scenario_id = static_cast<int32_t>(g->scenarios.size() - 1);
     });
+}
+
+namespace {
+mgb::InterferenceSchedule schedule_from(const migsim_schedule_desc& d) {
+    mgb::InterferenceSchedule s;
+    if (d.kind < 0 || d.kind > 2) throw mgb::ConfigError("unknown schedule kind " + std::to_string(d.kind), "<spec>");
+    s.kind = static_cast<mgb::InterferenceSchedule::Kind>(d.kind);
+    s.period_s = d.period_s;
+    s.duty = d.duty;
+    s.offset_s = d.offset_s;
+    for (size_t k = 0; k < d.n_phases; ++k) s.phases.push_back({d.phase_start_s[k], d.phase_end_s[k]});
+    return s;
+}
+
+// migsim_scenario_desc -> the engine's host ScenarioSpec, field for field (scenario.hpp:30-61)
+mgb::ScenarioSpec spec_from(const migsim_scenario_desc& d) {
+    mgb::ScenarioSpec s;
+    s.name = d.name ? d.name : "";
+    s.duration_s = d.duration_s;
+    s.measure_start_s = d.measure_start_s;
+    s.fabric_redistribute = d.fabric_redistribute != 0;
+    for (size_t h = 0; h < d.n_hosts; ++h) {
+        const migsim_host_desc& hd = d.hosts[h];
+        mgb::HostSpec host;
+        for (size_t k = 0; k < hd.n_gpus; ++k) {
+            const migsim_gpu_desc& gd = hd.gpus[k];
+            host.gpus.push_back({gd.id, gd.pcie_root_id, gd.numa_id, gd.core_group, gd.total_slices, gd.mig_enabled != 0});
+        }
+        host.numa_domains = hd.numa_domains;
+        for (size_t k = 0; k < hd.n_roots; ++k) host.pcie_roots.push_back({hd.roots[k].id, hd.roots[k].capacity_Bps});
+        for (size_t k = 0; k < hd.n_irq_hot; ++k) host.irq_hot_core_groups.insert(hd.irq_hot_core_groups[k]);
+        host.io_capacity_Bps = hd.io_capacity_Bps;
+        s.topology.hosts.push_back(std::move(host));
+    }
+    for (size_t i = 0; i < d.n_tenants; ++i) {
+        const migsim_tenant_desc& td = d.tenants[i];
+        mgb::TenantEntry e;
+        if (!td.id) throw mgb::ConfigError("tenant " + std::to_string(i) + " has no id", "<spec>");
+        e.spec.id = td.id;
+        if (td.tclass < 0 || td.tclass > 2) throw mgb::ConfigError("unknown tenant class " + std::to_string(td.tclass), "<spec>");
+        e.spec.tclass = static_cast<mgb::TenantClass>(td.tclass);
+        e.spec.arrival_rate_hz = td.arrival_rate_hz;
+        e.spec.arrival_cv = td.arrival_cv;
+        for (size_t k = 0; k < td.n_mix; ++k) e.spec.transfer_mix.push_back({td.mix_bytes[k], td.mix_weight[k]});
+        e.spec.base_compute_ms = td.base_compute_ms;
+        e.spec.service_cv = td.service_cv;
+        e.spec.slo_tail_ms = td.slo_tail_ms;
+        e.spec.weight = td.weight;
+        e.spec.pcie_cap_Bps = td.pcie_cap_Bps;
+        e.spec.host_io_Bps = td.host_io_Bps;
+        e.spec.sm_demand = td.sm_demand;
+        e.spec.noise_mean_ms = td.noise_mean_ms;
+        e.placement = {td.host, td.gpu, {td.first_slice, td.slice_count}};
+        e.profile_name = td.profile ? td.profile : "";
+        e.schedule = schedule_from(td.schedule);
+        s.tenants.push_back(std::move(e));
+    }
+    for (size_t k = 0; k < d.n_irq_bursts; ++k) {
+        const migsim_irq_desc& id = d.irq_bursts[k];
+        s.irq_bursts.push_back({id.host, id.core_group, id.extra_noise_ms, schedule_from(id.schedule)});
+    }
+    const migsim_controller_desc& c = d.controller;
+    mgb::ControllerConfig& o = s.controller;
+    o.enabled = c.enabled != 0;
+    o.enable_mig = c.enable_mig != 0;
+    o.enable_placement = c.enable_placement != 0;
+    o.enable_guardrails = c.enable_guardrails != 0;
+    o.tail_threshold_ms = c.tail_threshold_ms;
+    o.persistence_windows = c.persistence_windows;
+    o.dwell_obs = c.dwell_obs;
+    o.cooldown_obs = c.cooldown_obs;
+    o.sample_interval_s = c.sample_interval_s;
+    o.warmup_s = c.warmup_s;
+    o.move_futility_ratio = c.move_futility_ratio;
+    o.throttle_duration_s = c.throttle_duration_s;
+    o.quota_duration_s = c.quota_duration_s;
+    o.ema_alpha = c.ema_alpha;
+    o.hysteresis_clear_ratio = c.hysteresis_clear_ratio;
+    o.relax_stability_ratio = c.relax_stability_ratio;
+    o.relax_score_threshold = c.relax_score_threshold;
+    o.validation_obs = c.validation_obs;
+    o.rollback_regress_ratio = c.rollback_regress_ratio;
+    o.diag_pcie_util_threshold = c.diag_pcie_util_threshold;
+    o.diag_host_io_threshold = c.diag_host_io_threshold;
+    o.diag_sm_util_threshold = c.diag_sm_util_threshold;
+    o.move_margin = c.move_margin;
+    o.admission_queue_timeout_epochs = c.admission_queue_timeout_epochs;
+    o.guardrail_io_throttle_Bps = c.guardrail_io_throttle_Bps;
+    o.guardrail_mps_quota_pct = c.guardrail_mps_quota_pct;
+    o.irq_lookback_s = c.irq_lookback_s;
+    o.throughput_floor = c.throughput_floor;
+    s.validate();
+    return s;
+}
+}  // namespace
+
+int migsim_gpu_load_spec(migsim_gpu* g, const migsim_scenario_desc* spec, int32_t* scenario_id, char* err,
+                         size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (!g || !spec || !scenario_id) throw std::runtime_error("null argument");
+        g->scenarios.push_back(spec_from(*spec));
+        *scenario_id = static_cast<int32_t>(g->scenarios.size() - 1);
+    });
+}
+
+int migsim_gpu_release_scenario(migsim_gpu* g, int32_t id) {
+    if (!g || id < 0 || id >= static_cast<int32_t>(g->scenarios.size())) return MIGSIM_ERR_CONFIG;
+    g->scenarios[static_cast<size_t>(id)] = mgb::ScenarioSpec{};
+    g->released.resize(g->scenarios.size(), 0);
+    g->released[static_cast<size_t>(id)] = 1;
+    return MIGSIM_OK;
 }
 
 int migsim_gpu_load_scenario_file(migsim_gpu* g, const char* path, int32_t* scenario_id, char* err, size_t errlen) {
@@ -661,8 +951,7 @@ int migsim_gpu_run_batch(migsim_gpu* g, int32_t scenario_id, const migsim_varian
                          const uint64_t* seeds, size_t n_seeds, const migsim_run_opts* opts, migsim_batch_result** out,
                          char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
-        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
-            throw mgb::ConfigError("unknown scenario id");
+        check_scenario_id(g, scenario_id);
         if (n_seeds == 0) throw mgb::ConfigError("experiment needs at least one seed");
         std::vector<mgb::Variant> vs;
         for (size_t i = 0; i < n_variants; ++i) vs.push_back(to_variant(variants[i]));
@@ -679,8 +968,7 @@ int migsim_gpu_run_batch(migsim_gpu* g, int32_t scenario_id, const migsim_varian
 int migsim_gpu_run_scenario(migsim_gpu* g, int32_t scenario_id, const migsim_variant* variant, uint64_t seed,
                             const char* out_dir, int32_t write_traces, char** result_json, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
-        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
-            throw mgb::ConfigError("unknown scenario id");
+        check_scenario_id(g, scenario_id);
         const std::string dir = out_dir ? out_dir : "";
         std::vector<mgb::Variant> vs(1);
         if (variant) vs[0] = to_variant(*variant);
@@ -767,6 +1055,15 @@ int64_t migsim_batch_completions(const migsim_batch_result* r, size_t run, doubl
 }
 
 void migsim_batch_result_free(migsim_batch_result* r) { delete r; }
+
+int64_t migsim_batch_completion_records(const migsim_batch_result* r, size_t run, migsim_completion* out, int64_t cap) {
+    if (!r || run >= r->n_runs || r->crec_off.empty()) return -1;
+    const int64_t a = r->crec_off[run], b = r->crec_off[run + 1];
+    if (!out) return b - a;
+    const int64_t n = std::min(cap, b - a);
+    if (n > 0) std::memcpy(out, r->crec.data() + a, sizeof(migsim_completion) * static_cast<size_t>(n));
+    return b - a;
+}
 
 size_t migsim_batch_n_variants(const migsim_batch_result* r) { return r ? r->variants.size() : 0; }
 
@@ -941,8 +1238,7 @@ int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n, const int32_t
                      const uint32_t* irq_recent, migsim_admit_decision* out, double* device_ms, char* err,
                      size_t errlen) {
     return guarded(err, errlen, [&] {
-        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
-            throw mgb::ConfigError("unknown scenario id");
+        check_scenario_id(g, scenario_id);
         CK(cudaSetDevice(g->device));
         const mgb::ScenarioSpec& spec = g->scenarios[static_cast<size_t>(scenario_id)];
         const mgb::Packed P = mgb::pack(spec, {});
@@ -1125,8 +1421,7 @@ int migsim_gpu_libm(migsim_gpu* g, int fn, const double* x, const double* y, dou
 int migsim_gpu_arrivals(migsim_gpu* g, int32_t scenario_id, uint64_t seed, int32_t tenant, double* out, int64_t cap,
                         int64_t* n_out, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
-        if (!g || scenario_id < 0 || scenario_id >= static_cast<int32_t>(g->scenarios.size()))
-            throw mgb::ConfigError("unknown scenario id");
+        check_scenario_id(g, scenario_id);
         CK(cudaSetDevice(g->device));
         const mgb::Packed P = mgb::pack(g->scenarios[static_cast<size_t>(scenario_id)], {});
         const int T = P.scen.n_tenants;

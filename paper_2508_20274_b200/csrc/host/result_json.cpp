@@ -59,7 +59,8 @@ std::string result_to_json(const RunResult& r) {
         if (!first) o += ",";
         first = false;
         o += str(id) + ":{\"host\":" + num(e.placement.host) + ",\"gpu\":" + num(e.placement.gpu) +
-             ",\"first_slice\":" + num(e.placement.slices.first) + ",\"profile\":" + str(e.profile) +
+             ",\"first_slice\":" + num(e.placement.slices.first) +
+             ",\"slice_count\":" + num(e.placement.slices.count) + ",\"profile\":" + str(e.profile) +
              ",\"claim_Bps\":" + num(e.claim_Bps) + ",\"status\":\"admitted\",\"cpu_pinned\":" +
              (e.cpu_pinned ? "true" : "false") + "}";
     }

@@ -6,7 +6,10 @@ collectives run (torch.distributed: NCCL over NVLink on the GPU box, gloo in the
   * all-reduce (sum, int64) of the per-variant SLO-miss-rate histogram (1e-3 bins on [0, 1]);
   * all-gather of the per-seed focus rows (p99, miss rate, summed throughput) so rank 0 can
     build harness-identical confidence intervals by summing in seed order
-    (harness.cpp:32-43, 178-204).
+    (harness.cpp:32-43, 178-204);
+  * all-reduce (sum, int64) of the per-(variant, tenant) window-latency histograms (lat_hist.h
+    bins, summed over seeds on the device) and the per-(variant, tenant) completion / window /
+    SLO-miss counters (engine.cpp:497-501, 797-798).  Integer, so exact and order-independent.
 """
 from __future__ import annotations
 
@@ -86,3 +89,21 @@ def reduce_rows(rows: np.ndarray, dist=None, device: str = "cpu"):
     all_rows = local.cpu().numpy()
     cis = [confidence_interval(all_rows[:, k]) for k in range(3)]
     return all_rows, hist.cpu().numpy(), cis
+
+
+def reduce_tenant_hists(lat_hist: np.ndarray, counts: np.ndarray, dist=None, device: str = "cpu"):
+    """lat_hist: int64 [n_variants, n_tenants, bins]; counts: int64 [n_variants, n_tenants, 3]
+    (completed_total, completed_window, window_misses), this rank's sums over its seeds.
+
+    One all-reduce (sum) of both, packed into a single int64 buffer; returns the global sums on
+    every rank.  Every rank must pass the same shapes (same scenario and variants)."""
+    import torch
+
+    lat_hist = np.ascontiguousarray(lat_hist, np.int64)
+    counts = np.ascontiguousarray(counts, np.int64)
+    if dist is None or not dist.is_initialized() or dist.get_world_size() <= 1:
+        return lat_hist.copy(), counts.copy()
+    buf = torch.from_numpy(np.concatenate([lat_hist.ravel(), counts.ravel()])).to(device)
+    dist.all_reduce(buf)
+    out = buf.cpu().numpy()
+    return out[: lat_hist.size].reshape(lat_hist.shape), out[lat_hist.size:].reshape(counts.shape)

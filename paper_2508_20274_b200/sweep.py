@@ -24,7 +24,7 @@ from typing import Dict, List, Optional, Sequence
 import numpy as np
 
 from . import sharding
-from .api import Engine, Variant, ablation_variants, main_variants, scenario_spec
+from .api import HIST_BINS, Engine, Variant, ablation_variants, main_variants, scenario_spec
 
 
 def focus_rows(res, focus: str) -> np.ndarray:
@@ -63,20 +63,27 @@ def run_sweep(path: str, variants: Sequence[Variant], seeds: Sequence[int], focu
     t0 = time.perf_counter()
     for v in variants:
         rows = []
+        lat = np.zeros((1, T, HIST_BINS), np.int64)
+        cnt = np.zeros((1, T, 3), np.int64)
         for c0 in range(0, len(seeds), chunk):
             part = list(seeds[c0:c0 + chunk])
             res = eng.run_batch(sid, part, [v])
             rows.append(focus_rows(res, focus))
+            lat += res.latency_hist()
+            cnt += res.tenant_counts()
             out["tenant_ticks"] += int(res.timing["tenant_ticks"])
             out["device_ms"] += float(res.timing["total_device_ms"])
             out["completions"] += int(res.timing["completions"])
             res.close()
         local = np.concatenate(rows, 0) if rows else np.zeros((0, 3))
         all_rows, hist, cis = sharding.reduce_rows(local, dist, device=coll_device)
+        lat, cnt = sharding.reduce_tenant_hists(lat, cnt, dist, device=coll_device)
         out["variants"].append({"name": v.name, "seeds": int(all_rows.shape[0]), "p99_ci": cis[0], "miss_ci": cis[1],
-                                "throughput_ci": cis[2], "miss_histogram": hist, "rows": all_rows})
+                                "throughput_ci": cis[2], "miss_histogram": hist, "rows": all_rows,
+                                "latency_hist": lat[0], "tenant_counts": cnt[0]})
     out["wall_s"] = time.perf_counter() - t0
     out["tenants"] = T
+    out["tenant_ids"] = eng.tenant_ids(sid)
     eng.close()
     return out
 
@@ -140,6 +147,9 @@ def main(argv=None) -> None:
             "tenant_ticks_per_s": res["tenant_ticks"] / (res["device_ms"] / 1e3) if res["device_ms"] else None,
             "variants": [{"name": v["name"], "seeds": v["seeds"], "p99_ci": v["p99_ci"], "miss_ci": v["miss_ci"],
                           "throughput_ci": v["throughput_ci"],
+                          "tenant_counts": {tid: [int(x) for x in v["tenant_counts"][i]]
+                                            for i, tid in enumerate(res["tenant_ids"])},
+                          "latency_hist_total": int(v["latency_hist"].sum()),
                           "miss_histogram_nonzero": {int(i): int(x) for i, x in enumerate(v["miss_histogram"]) if x}}
                          for v in res["variants"]],
         }

@@ -243,3 +243,29 @@ def test_hist_bin_edges_match_restated_bins():
     assert (restate.lat_bins(below) == np.arange(HIST_BINS - 1)).all()
     # octave structure: 64 bins per doubling
     assert lo[64] == 2.0 ** -9 and lo[640] == 1.0
+
+
+def test_shim_binaries_fail_loudly_without_gpu(tmp_path):
+    """The reference linked against the B200 shim (oracle/_ref/shim_parity) has no CPU fallback:
+    without a device the shim's engine::run_scenario raises, the binary reports it and exits 1."""
+    import os
+    import subprocess
+
+    import pytest as _pt
+
+    from oracle.json_scenarios import write_dir
+    from tests._libs import GOLDEN_SCENARIOS, ROOT
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "shim_parity")
+    if not os.path.exists(exe):
+        _pt.skip("shim binaries are built only where /root/reference is mounted")
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            _pt.skip("a GPU is present")
+    except ImportError:
+        pass
+    d = write_dir(str(tmp_path), GOLDEN_SCENARIOS[:1])
+    p = subprocess.run([exe, "spec", os.path.join(d, "default.yaml")], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 1 and "ERROR migsim-b200" in p.stdout, p.stdout + p.stderr

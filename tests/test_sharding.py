@@ -90,3 +90,39 @@ def test_uneven_split_reduction(n, world):
         all_rows, hist, cis = out[r]
         assert all_rows.shape == rows.shape and (all_rows == rows).all()
         assert (hist == single_hist).all() and cis == single_cis
+
+
+def _hist_worker(rank, world, port, lat_all, cnt_all, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seeds = sharding.split_seeds(list(range(lat_all.shape[0])), rank, world)
+    lat = lat_all[seeds].sum(0) if seeds else np.zeros(lat_all.shape[1:], np.int64)
+    cnt = cnt_all[seeds].sum(0) if seeds else np.zeros(cnt_all.shape[1:], np.int64)
+    out[rank] = sharding.reduce_tenant_hists(lat, cnt, dist)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_seeds", [7, 1])
+def test_two_rank_tenant_hists_equal_single_rank(n_seeds):
+    """Per-(variant, tenant) latency histograms + completion/miss counters: the 2-rank all-reduce of
+    per-seed-block sums equals the 1-rank sum (uneven and empty seed blocks included)."""
+    rng = np.random.default_rng(11)
+    lat_all = rng.integers(0, 1 << 40, size=(n_seeds, 3, 4, 2048), dtype=np.int64)
+    cnt_all = rng.integers(0, 1 << 40, size=(n_seeds, 3, 4, 3), dtype=np.int64)
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_hist_worker, args=(r, 2, port, lat_all, cnt_all, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    one = sharding.reduce_tenant_hists(lat_all.sum(0), cnt_all.sum(0), None)
+    for r in range(2):
+        lat, cnt = out[r]
+        assert lat.dtype == np.int64 and (lat == one[0]).all() and (cnt == one[1]).all()

@@ -239,7 +239,11 @@ MIGSIM_API int migsim_gpu_select(migsim_gpu* g, const double* vals, const int64_
  * case c requests tenant tenant[c] at MIG profile profile[c] (lattice index 0..4 = 1g..7g) given
  * TenantStates admitted/host/gpu_id/first/count [n][T] and the ClusterSnapshot fields the scoring
  * reads: tenant_pcie_Bps, tenant_host_io_Bps [n][T] and irq_recent [n][n_hosts] (bit g = core
- * group g of that host had a recent IRQ burst).  A fresh controller is assumed (first retry).
+ * group g of that host had a recent IRQ burst).  queue_epochs [n] (in/out, may be NULL = fresh
+ * controllers) is the case's controller state Controller::queue_epochs_[tenant] (controller.hpp:
+ * 214; 0 = no entry): a request without a feasible slot increments it and is rejected (entry
+ * erased) once it exceeds admission_queue_timeout_epochs, an admitted request erases it
+ * (controller.cpp:671-691) -- carry the array across calls to retry queued requests.
  * outcome: 0 admitted, 1 queued, 2 rejected; reason: 0 none, 1 service rate, 2 no feasible slot,
  * 3 queue timeout. */
 typedef struct migsim_admit_decision {
@@ -249,7 +253,8 @@ typedef struct migsim_admit_decision {
 MIGSIM_API int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n_cases, const int32_t* tenant,
                      const int32_t* profile, const int32_t* admitted, const int32_t* host, const int32_t* gpu_id,
                      const int32_t* first, const int32_t* count, const double* tenant_pcie_Bps,
-                     const double* tenant_host_io_Bps, const uint32_t* irq_recent, migsim_admit_decision* out,
+                     const double* tenant_host_io_Bps, const uint32_t* irq_recent, int32_t* queue_epochs,
+                     migsim_admit_decision* out,
                      double* device_ms, char* err, size_t errlen);
 
 /* Batched experiment plans (harness::run_plan, harness.cpp:114-216; PlanOptions harness.hpp:84-92):

@@ -297,10 +297,12 @@ char* ref_render_report(const char* experiment_json_text) {
 // id) order, states [n][T] (admitted, host, gpu id, first, count), snapshot fields [n][T] and
 // irq_recent [n][H] bitmasks, request (tenant index, lattice index).  A fresh Controller per case.
 // out: [n][6] ints (outcome 0/1/2, host, gpu, first, count, reason code) and score[n].
-int ref_admit(const char* scenario_json, int n, const int32_t* tenant, const int32_t* profile,
-              const int32_t* admitted, const int32_t* host, const int32_t* gpu_id, const int32_t* first,
-              const int32_t* count, const double* pcie, const double* hio, const uint32_t* irq, int32_t* out,
-              double* score) {
+// ref_admit_repeat: the same request `repeat` times on ONE controller per case (its queue_epochs_
+// carries across the calls, controller.cpp:671-691); out/score hold [n][repeat] decisions.
+int ref_admit_repeat(const char* scenario_json, int n, const int32_t* tenant, const int32_t* profile,
+                     const int32_t* admitted, const int32_t* host, const int32_t* gpu_id, const int32_t* first,
+                     const int32_t* count, const double* pcie, const double* hio, const uint32_t* irq, int repeat,
+                     int32_t* out, double* score) {
     try {
         const auto spec = scenario::parse_scenario(scenario_json, "<scenario>");
         std::vector<const scenario::TenantEntry*> canon;
@@ -330,8 +332,10 @@ int ref_admit(const char* scenario_json, int n, const int32_t* tenant, const int
                 for (int g = 0; g < 32; ++g)
                     if ((irq[c * H + h] >> g) & 1u) snap.irq_recent.insert({h, g});
             control::Controller ctl(spec.controller, spec.topology);
+            for (int rep = 0; rep < repeat; ++rep) {
+            const int oc = c * repeat + rep;
             const auto d = ctl.admit(canon[tenant[c]]->spec, lattice[profile[c]].name, snap, states);
-            int32_t* o = out + 6 * c;
+            int32_t* o = out + 6 * oc;
             o[0] = d.outcome == control::AdmissionOutcome::admitted ? 0
                    : d.outcome == control::AdmissionOutcome::queued ? 1 : 2;
             o[1] = o[0] == 0 ? d.placement.host : -1;
@@ -341,16 +345,25 @@ int ref_admit(const char* scenario_json, int n, const int32_t* tenant, const int
             o[5] = o[0] == 0 ? 0
                    : d.reason.find("service rate") != std::string::npos ? 1
                    : d.reason.find("timeout") != std::string::npos ? 3 : 2;
-            score[c] = 0.0;
+            score[oc] = 0.0;
             if (o[0] == 0)
-                score[c] = control::placement_score(spec.topology, states, snap, canon[tenant[c]]->spec.id,
-                                                    d.placement.host, d.placement.gpu).total();
+                score[oc] = control::placement_score(spec.topology, states, snap, canon[tenant[c]]->spec.id,
+                                                     d.placement.host, d.placement.gpu).total();
+            }
         }
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
         return 1;
     }
+}
+
+int ref_admit(const char* scenario_json, int n, const int32_t* tenant, const int32_t* profile,
+              const int32_t* admitted, const int32_t* host, const int32_t* gpu_id, const int32_t* first,
+              const int32_t* count, const double* pcie, const double* hio, const uint32_t* irq, int32_t* out,
+              double* score) {
+    return ref_admit_repeat(scenario_json, n, tenant, profile, admitted, host, gpu_id, first, count, pcie, hio, irq, 1,
+                            out, score);
 }
 
 const char* ref_result_json(void* hp) { return static_cast<Handle*>(hp)->json_text.c_str(); }

@@ -158,7 +158,7 @@ def load_library() -> ctypes.CDLL:
                                             ctypes.c_int32, ctypes.POINTER(vp), cp, sz]
     lib.migsim_run_plan.argtypes = [vp, cp, cp, ctypes.c_int32, ctypes.c_uint64, cp, cp, ctypes.POINTER(vp), cp, sz]
     lib.migsim_render_report.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
-    lib.migsim_gpu_admit.argtypes = [vp, ctypes.c_int32, sz] + [vp] * 11 + [ctypes.POINTER(ctypes.c_double), cp, sz]
+    lib.migsim_gpu_admit.argtypes = [vp, ctypes.c_int32, sz] + [vp] * 12 + [ctypes.POINTER(ctypes.c_double), cp, sz]
     lib.migsim_free.argtypes = [vp]
     lib.migsim_scenario_dump.argtypes = [cp, ctypes.POINTER(vp), cp, sz]
     lib.migsim_batch_n_variants.argtypes = [vp]
@@ -385,14 +385,18 @@ class Engine:
             self._lib.migsim_free(out)
 
     def admit(self, sid: int, tenant, profile, admitted, host, gpu, first, count, tenant_pcie_Bps,
-              tenant_host_io_Bps, irq_recent) -> (np.ndarray, float):
+              tenant_host_io_Bps, irq_recent, queue_epochs: Optional[np.ndarray] = None) -> (np.ndarray, float):
         """Controller::admit (controller.cpp:637-692) for n independent cases on the GPU.
 
         tenant/profile: [n] canonical tenant index / MIG lattice index of each request;
         admitted/host/gpu/first/count and tenant_pcie_Bps/tenant_host_io_Bps: [n, T] TenantStates and
         snapshot fields (tenants in canonical order); irq_recent: [n, n_hosts] core-group bitmasks.
         Returns (decisions, device_ms); decisions has fields outcome (0 admitted, 1 queued,
-        2 rejected), host, gpu, first, count, profile, reason, score."""
+        2 rejected), host, gpu, first, count, profile, reason, score.
+
+        queue_epochs: optional int32 [n], each case's controller queue_epochs_[tenant] (0 = none),
+        updated IN PLACE (controller.cpp:671-691) -- pass the same array again to retry; None =
+        fresh controllers."""
         i32 = lambda a: np.ascontiguousarray(np.asarray(a, np.int32))  # noqa: E731
         f64 = lambda a: np.ascontiguousarray(np.asarray(a, np.float64))  # noqa: E731
         args = [i32(tenant), i32(profile), i32(admitted), i32(host), i32(gpu), i32(first), i32(count),
@@ -401,7 +405,12 @@ class Engine:
         out = np.zeros(n, dtype=ADMIT_DTYPE)
         ms = ctypes.c_double()
         err = ctypes.create_string_buffer(1024)
-        _check(self._lib.migsim_gpu_admit(self._h, sid, n, *[a.ctypes.data for a in args], out.ctypes.data,
+        if queue_epochs is not None:
+            if not (isinstance(queue_epochs, np.ndarray) and queue_epochs.dtype == np.int32
+                    and queue_epochs.flags.c_contiguous and queue_epochs.shape == (n,)):
+                raise ValueError("queue_epochs must be a contiguous int32 array of shape (n,)")
+        qe = queue_epochs.ctypes.data if queue_epochs is not None else None
+        _check(self._lib.migsim_gpu_admit(self._h, sid, n, *[a.ctypes.data for a in args], qe, out.ctypes.data,
                                           ctypes.byref(ms), err, 1024), err)
         return out, ms.value
 

@@ -155,20 +155,37 @@ MG_HD void tw_rebuild(TailWin& w) {
     }
 }
 
-// j-th largest (0-based) of `n` values in vals, full scan selection (validation window, fallback)
-MG_HD double select_jth_largest(const double* vals, int n, int j) {
-    // count-based selection: the value v with #(> v) <= j < #(>= v)
-    for (int a = 0; a < n; ++a) {
-        const double v = vals[a];
-        int gt = 0, ge = 0;
-        for (int b = 0; b < n; ++b) {
-            gt += vals[b] > v;
-            ge += vals[b] >= v;
-        }
-        if (gt <= j && j < ge) return v;
-    }
-    return vals[0];
+// j-th largest (0-based) of n values ring[(head + i) % cap], i < n -- the order statistic that
+// std::sort + nearest rank picks (telemetry.cpp:38-56, controller.cpp:446).  Bitwise bisection on
+// the order-preserving 64-bit keys: after 64 counting passes K is the largest key with at least
+// j+1 values >= K, i.e. exactly the j-th largest.  O(64 n), no scratch memory (used where the
+// cached top-K does not reach the rank: validation verdicts and windows longer than ~8/(1-q)).
+MG_HD uint64_t order_key(double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, 8);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
+MG_HD double from_order_key(uint64_t k) {
+    const uint64_t b = (k >> 63) ? (k & ~0x8000000000000000ull) : ~k;
+    double x;
+    std::memcpy(&x, &b, 8);
+    return x;
+}
+MG_HD double ring_jth_largest(const double* ring, int cap, int head, int n, int j) {
+    uint64_t K = 0;
+    for (int bit = 63; bit >= 0; --bit) {
+        const uint64_t c = K | (1ull << bit);
+        int cnt = 0;
+        int idx = head;
+        for (int i = 0; i < n; ++i) {
+            cnt += order_key(ring[idx]) >= c;
+            idx = idx + 1 == cap ? 0 : idx + 1;
+        }
+        if (cnt >= j + 1) K = c;
+    }
+    return from_order_key(K);
+}
+MG_HD double select_jth_largest(const double* vals, int n, int j) { return ring_jth_largest(vals, n, 0, n, j); }
 
 // nearest rank index from the top: rank = clamp(ceil(q*n), 1, n) (telemetry.cpp:52-55)
 MG_HD int nr_from_top(double q, int n) {
@@ -185,28 +202,8 @@ MG_HD double tw_quantile(TailWin& w, double q) {
         tw_rebuild(w);
         return w.top[j];
     }
-    // generic fallback (q far below the tail): selection over the ring in place
-    double best = 0.0;
-    {
-        // selection over the ring in place
-        for (int a = 0; a < w.n; ++a) {
-            int ia = w.head + a;
-            if (ia >= w.cap) ia -= w.cap;
-            const double v = w.ring[ia];
-            int gt = 0, ge = 0;
-            for (int b = 0; b < w.n; ++b) {
-                int ib = w.head + b;
-                if (ib >= w.cap) ib -= w.cap;
-                gt += w.ring[ib] > v;
-                ge += w.ring[ib] >= v;
-            }
-            if (gt <= j && j < ge) {
-                best = v;
-                break;
-            }
-        }
-    }
-    return best;
+    // rank beyond the cache (q far below the tail, or windows longer than ~8/(1-q)): linear selection
+    return ring_jth_largest(w.ring, w.cap, w.head, w.n, j);
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -256,13 +256,14 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     if (W == 0) W = 1;
 
     // ---- wave slots ------------------------------------------------------------------------
-    // Large batches run as a two-slot pipeline on two streams: the arrival generator of wave k+1
-    // and its event loop start while wave k's event loop drains (its ragged tail of long-running
-    // replicas), and wave k's host-side assembly overlaps wave k+1 on the device.  Small batches
-    // (one wave) and the keep_completions / traces paths (synchronous per-run copies) use one slot.
+    // MIGSIM_PIPELINE=1: multi-wave batches run as a two-slot pipeline on two streams (the
+    // generator of wave k+1 and its event loop start while wave k's event loop drains; wave k's
+    // host-side assembly overlaps wave k+1).  Off by default: measured 12.0 vs 12.5 M tenant-ticks/s
+    // on 16,384 default.yaml replicas (the half-size waves cost more than the overlap recovers;
+    // DESIGN.md section 6).  keep_completions / traces always use one slot.
     const bool want_prof = std::getenv("MIGSIM_PROFILE_EVENTS") != nullptr;
     const char* pipe_env = std::getenv("MIGSIM_PIPELINE");
-    const bool pipe_allowed = !(pipe_env && std::string(pipe_env) == "0") && !keep && !want_prof;
+    const bool pipe_allowed = pipe_env && std::string(pipe_env) == "1" && !keep && !want_prof;
     const int n_slots = (pipe_allowed && n_jobs > W) ? 2 : 1;
     if (n_slots == 2) W = std::max<size_t>(1, W / 2);
     WaveAlloc& A = g->wave[0];  // also holds the batch-wide buffers (scenario, controllers, histograms)
@@ -1235,8 +1236,8 @@ void migsim_free(void* p) { std::free(p); }
 int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n, const int32_t* tenant, const int32_t* profile,
                      const int32_t* admitted, const int32_t* host, const int32_t* gpu_id, const int32_t* first,
                      const int32_t* count, const double* tenant_pcie_Bps, const double* tenant_host_io_Bps,
-                     const uint32_t* irq_recent, migsim_admit_decision* out, double* device_ms, char* err,
-                     size_t errlen) {
+                     const uint32_t* irq_recent, int32_t* queue_epochs, migsim_admit_decision* out, double* device_ms,
+                     char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         check_scenario_id(g, scenario_id);
         CK(cudaSetDevice(g->device));
@@ -1261,7 +1262,7 @@ int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n, const int32_t
             }
         }
         DevBuf<mg::PScenario> dS;
-        DevBuf<int32_t> dt, dp, da, dh, dg, df, dc;
+        DevBuf<int32_t> dt, dp, da, dh, dg, df, dc, dq;
         DevBuf<double> dpc, dio;
         DevBuf<uint32_t> dirq;
         DevBuf<mg::AdmitOut> dout;
@@ -1282,8 +1283,9 @@ int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n, const int32_t
         up(dpc, tenant_pcie_Bps, n * T);
         up(dio, tenant_host_io_Bps, n * T);
         up(dirq, irq_recent, n * H);
+        if (queue_epochs) up(dq, queue_epochs, n);
         dout.alloc(n ? n : 1);
-        mg::AdmitCases C{dt.p, dp.p, da.p, dh.p, dg.p, df.p, dc.p, dpc.p, dio.p, dirq.p};
+        mg::AdmitCases C{dt.p, dp.p, da.p, dh.p, dg.p, df.p, dc.p, dpc.p, dio.p, dirq.p, queue_epochs ? dq.p : nullptr};
         CK(cudaEventRecord(g->ev[4], s));
         if (n) mg::admit_kernel<<<static_cast<unsigned>(n), 32, 0, s>>>(dS.p, C, static_cast<int>(n),
                                                                        spec.controller.admission_queue_timeout_epochs, dout.p);
@@ -1291,6 +1293,7 @@ int migsim_gpu_admit(migsim_gpu* g, int32_t scenario_id, size_t n, const int32_t
         CK(cudaEventRecord(g->ev[5], s));
         std::vector<mg::AdmitOut> h(n);
         if (n) CK(cudaMemcpyAsync(h.data(), dout.p, sizeof(mg::AdmitOut) * n, cudaMemcpyDeviceToHost, s));
+        if (n && queue_epochs) CK(cudaMemcpyAsync(queue_epochs, dq.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         float ms = 0;
         CK(cudaEventElapsedTime(&ms, g->ev[4], g->ev[5]));

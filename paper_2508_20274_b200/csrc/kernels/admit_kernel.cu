@@ -10,8 +10,10 @@
 //   score         placement_score(...).total() (controller.cpp:101-123): PCIe share of bandwidth-
 //                 heavy neighbours on the root + NUMA-local host I/O share + recent IRQ (0/1)
 //   choice        minimum score, ties to the smaller (host, gpu id, first)  (controller.cpp:662-668)
-//   no slot       a fresh controller's first retry: queued, or rejected when the queue timeout is
-//                 < 1 epoch (controller.cpp:677-691)
+//   no slot       queue_epochs_[tenant] += 1; rejected (entry erased) once it exceeds
+//                 admission_queue_timeout_epochs, else queued (controller.cpp:677-691); an admitted
+//                 request erases the entry (:671).  The per-case epochs are in/out, so a caller can
+//                 carry each controller's queue across calls (retry epochs).
 // All sums run in the reference's order with IEEE division (no FMA contraction: --fmad=false), so
 // outcomes, placements and scores are bit-identical to the reference.
 #include "admit_kernel.cuh"
@@ -131,12 +133,18 @@ __global__ void __launch_bounds__(32) admit_kernel(const PScenario* __restrict__
         o.first = bf;
         o.score = best;
         o.reason = kReasonNone;
-    } else if (1 > queue_timeout_epochs) {  // epochs == 1 for a fresh request
-        o.outcome = kAdmitRejected;
-        o.reason = kReasonTimeout;
+        if (C.queue_epochs) C.queue_epochs[c] = 0;  // queue_epochs_.erase (controller.cpp:671)
     } else {
-        o.outcome = kAdmitQueued;
-        o.reason = kReasonNoSlot;
+        int32_t epochs = (C.queue_epochs ? C.queue_epochs[c] : 0) + 1;
+        if (epochs > queue_timeout_epochs) {
+            o.outcome = kAdmitRejected;
+            o.reason = kReasonTimeout;
+            epochs = 0;  // erased with the rejection (controller.cpp:680-683)
+        } else {
+            o.outcome = kAdmitQueued;
+            o.reason = kReasonNoSlot;
+        }
+        if (C.queue_epochs) C.queue_epochs[c] = epochs;
     }
     out[c] = o;
 }

@@ -18,6 +18,8 @@ struct AdmitCases {
     const int32_t *admitted, *host, *gpu, *first, *count;  // [n][T] TenantStates
     const double *tenant_pcie, *tenant_host_io;             // [n][T] ClusterSnapshot::tenant_*_Bps
     const uint32_t* irq_recent;                             // [n][H] bit g: (host, core group g) recent
+    int32_t* queue_epochs;  // [n] in/out: the controller's queue_epochs_[tenant] (controller.hpp:214),
+                            // 0 = no entry; nullptr = a fresh controller
 };
 
 struct AdmitOut {

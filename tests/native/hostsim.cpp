@@ -279,4 +279,22 @@ void hostsim_math(int fn, const double* x, const double* y, double* out, long n)
         out[i] = fn == 0 ? mg::gl_log(x[i]) : fn == 1 ? mg::gl_exp(x[i]) : mg::gl_pow(x[i], y[i]);
 }
 
+// the engine's sliding window (des_core.h TailWin: cached top-K + linear selection beyond it):
+// out[i] = quantile(q) after push i, same contract as the oracle's ref_tailwindow_run
+void hostsim_tailwin_run(long capacity, const double* xs, long n, double q, double* out) {
+    std::vector<double> ring(static_cast<size_t>(capacity));
+    mg::TailWin w{};
+    w.ring = ring.data();
+    w.cap = static_cast<int32_t>(capacity);
+    mg::tw_reset(w, 1e300);
+    for (long i = 0; i < n; ++i) {
+        mg::tw_push(w, xs[i]);
+        out[i] = mg::tw_quantile(w, q);
+    }
+}
+
+double hostsim_select_jth(const double* v, long n, long j) {
+    return mg::select_jth_largest(v, static_cast<int>(n), static_cast<int>(j));
+}
+
 }  // extern "C"

@@ -269,3 +269,40 @@ def test_shim_binaries_fail_loudly_without_gpu(tmp_path):
     d = write_dir(str(tmp_path), GOLDEN_SCENARIOS[:1])
     p = subprocess.run([exe, "spec", os.path.join(d, "default.yaml")], capture_output=True, text=True, timeout=120)
     assert p.returncode == 1 and "ERROR migsim-b200" in p.stdout, p.stdout + p.stderr
+
+
+@pytest.mark.parametrize("cap,q", [(256, 0.99), (2048, 0.99), (1024, 0.5), (600, 0.95), (64, 0.0), (3000, 0.999)])
+def test_tailwin_any_rank_matches_reference(cap, q):
+    """The engine's window (cached top-8 + linear bisection select past it) equals the reference's
+    TailWindow (telemetry.cpp:30-56, copy + std::sort per query) for every push, including windows
+    far longer than the cache reaches (ranks 20+ below the top) and mid quantiles, with ties."""
+    import ctypes
+
+    from tests._libs import hostsim, oracle
+
+    rng = np.random.default_rng(cap)
+    n = 3 * cap + 17
+    xs = np.round(rng.lognormal(2.0, 0.8, n), 2)  # rounding creates ties
+    want = np.zeros(n)
+    got = np.zeros(n)
+    oracle().ref_tailwindow_run(cap, xs.ctypes.data, n, q, want.ctypes.data)
+    lib = hostsim()
+    lib.hostsim_tailwin_run.argtypes = [ctypes.c_long, ctypes.c_void_p, ctypes.c_long, ctypes.c_double, ctypes.c_void_p]
+    lib.hostsim_tailwin_run(cap, xs.ctypes.data, n, q, got.ctypes.data)
+    assert (want.view(np.uint64) == got.view(np.uint64)).all()
+
+
+def test_select_jth_largest_is_the_sorted_order_statistic():
+    import ctypes
+
+    from tests._libs import hostsim
+
+    lib = hostsim()
+    lib.hostsim_select_jth.argtypes = [ctypes.c_void_p, ctypes.c_long, ctypes.c_long]
+    lib.hostsim_select_jth.restype = ctypes.c_double
+    rng = np.random.default_rng(3)
+    for n in (1, 2, 7, 64, 256, 1000):
+        v = np.round(rng.exponential(5.0, n), 1)
+        s = np.sort(v)[::-1]
+        for j in {0, n // 3, n - 1}:
+            assert lib.hostsim_select_jth(v.ctypes.data, n, j) == s[j]

@@ -271,7 +271,8 @@ MIGSIM_API void migsim_free(void* p);
 /* Host-only: parse a scenario (path) with the engine's scenario-v1 loader and return the
  * normalised spec as JSON (no GPU needed). */
 MIGSIM_API int migsim_scenario_dump(const char* path, char** json, char* err, size_t errlen);
-/* Device glibc-exact math: fn 0 = log(x), 1 = exp(x), 2 = pow(x, y); n values. */
+/* Device glibc-exact math: fn 0 = log(x), 1 = exp(x), 2 = pow(x, y), 3 = fmod(x, y) (the
+ * schedule phase, arrivals.h sched_active); n values. */
 MIGSIM_API int migsim_gpu_libm(migsim_gpu* g, int fn, const double* x, const double* y, double* out, size_t n,
                                char* err, size_t errlen);
 /* Device-generated arrival records of one tenant (canonical index) for one seed:

@@ -33,6 +33,13 @@
 #if defined(__CUDA_ARCH__)
 #define MG_DEV_INLINE __device__ __forceinline__
 #endif
+// A/B switch (build flag -DMG_OUTLINE_HOT): the shared pipeline helpers as single out-of-line copies
+// instead of one inlined copy per call site (instruction-cache footprint of the event loop)
+#if defined(MG_OUTLINE_HOT) && defined(__CUDACC__)
+#define MG_HOT __host__ __device__ __noinline__
+#else
+#define MG_HOT MG_HD
+#endif
 
 namespace mg {
 
@@ -172,6 +179,26 @@ MG_HD double from_order_key(uint64_t k) {
     return x;
 }
 MG_HD double ring_jth_largest(const double* ring, int cap, int head, int n, int j) {
+    if (j < kTopK) {
+        // small rank (the p99 of windows up to ~800 samples, e.g. every validation verdict): one
+        // pass keeping the j+1 largest values, a sorted multiset -- the same order statistic
+        double top[kTopK];
+        int m = 0;
+        int idx = head;
+        for (int i = 0; i < n; ++i) {
+            const double x = ring[idx];
+            idx = idx + 1 == cap ? 0 : idx + 1;
+            if (m <= j || x > top[m - 1]) {
+                int k = m <= j ? m++ : m - 1;
+                while (k > 0 && top[k - 1] < x) {
+                    top[k] = top[k - 1];
+                    --k;
+                }
+                top[k] = x;
+            }
+        }
+        return top[j];
+    }
     uint64_t K = 0;
     for (int bit = 63; bit >= 0; --bit) {
         const uint64_t c = K | (1ull << bit);
@@ -489,7 +516,7 @@ struct Sim {
     }
 
     // ---- fabric (fabric.cpp:31-87 via engine.cpp:312-347) ----------------------------------
-    MG_HD void settle_root(int r) {
+    MG_HOT void settle_root(int r) {
         for (Mask m = static_cast<Mask>(rd[r].active); m; m &= m - 1) {
             TenantDyn& d = td[ctz64(m)];
             const double dt = fsub(now, d.last_settle);
@@ -502,7 +529,7 @@ struct Sim {
         }
     }
 
-    MG_HD void reallocate_root(int r) {
+    MG_HOT void reallocate_root(int r) {
         const Mask act = static_cast<Mask>(rd[r].active);
         const double cap = rt[r].capacity;
         if (act) {
@@ -572,7 +599,7 @@ struct Sim {
         return false;
     }
 
-    MG_HD void start_compute(int i) {
+    MG_HOT void start_compute(int i) {
         TenantDyn& d = td[i];
         const int cq_end = d.transferring ? d.tq_head - 1 : d.tq_head;
         if (d.computing || d.paused || d.cq_head >= cq_end) return;
@@ -618,7 +645,7 @@ struct Sim {
         push(kEvCompute, i, d.compute_end);
     }
 
-    MG_HD void start_transfer(int i) {
+    MG_HOT void start_transfer(int i) {
         TenantDyn& d = td[i];
         if (d.transferring || d.paused) return;
         const int64_t base = d.base;

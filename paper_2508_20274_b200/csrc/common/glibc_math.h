@@ -103,6 +103,33 @@ MG_HD double fdiv_exact(double a, double b) {
     return a / b;
 #endif
 }
+// C fmod(x, y) (exact in IEEE arithmetic: the result x - n*y, n = trunc(x/y), is representable),
+// without the library's bit-serial loop: n is estimated through a float reciprocal (relative error
+// < 2^-22, so off by at most one while |x/y| < 2^20) and corrected until the remainder lies in
+// [0, |y|).  For the correct n the FMA computes the exact remainder (representable => no
+// rounding); for a wrong n the rounded value still has the right sign / side of |y| (rounding is
+// monotone and |y| is representable), so the corrections are exact decisions.  Anything outside
+// the fast range (NaN, inf, y outside the float-normal range, huge quotients) takes the library fmod.
+MG_HD double fmod_fast(double x, double y) {
+    const double ax = fabs(x), ay = fabs(y);
+    if (!(ay >= 0x1p-120 && ay <= 0x1p120 && ax < fmul(ay, 0x1p20))) return fmod(x, y);  // float-normal y
+#if defined(__CUDA_ARCH__)
+    const double inv = static_cast<double>(__frcp_rn(__double2float_rn(ay)));
+#else
+    const double inv = static_cast<double>(1.0f / static_cast<float>(ay));
+#endif
+    double n = trunc(fmul(ax, inv));
+    double r = ffma(-n, ay, ax);
+    while (r < 0.0) {
+        n = fsub(n, 1.0);
+        r = ffma(-n, ay, ax);
+    }
+    while (r >= ay) {
+        n = fadd(n, 1.0);
+        r = ffma(-n, ay, ax);
+    }
+    return copysign(r, x);
+}
 MG_HD double fsqrt(double a) {
 #if defined(__CUDA_ARCH__)
     return __dsqrt_rn(a);

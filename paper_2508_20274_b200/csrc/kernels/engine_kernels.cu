@@ -483,7 +483,7 @@ __global__ void libm_kernel(int fn, const double* __restrict__ x, const double* 
                             int64_t n) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    out[i] = fn == 0 ? gl_log(x[i]) : fn == 1 ? gl_exp(x[i]) : gl_pow(x[i], y[i]);
+    out[i] = fn == 0 ? gl_log(x[i]) : fn == 1 ? gl_exp(x[i]) : fn == 2 ? gl_pow(x[i], y[i]) : fmod_fast(x[i], y[i]);
 }
 }  // namespace mg
 

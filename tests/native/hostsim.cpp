@@ -276,7 +276,8 @@ void hostsim_lat_bin(const double* x, uint32_t* bin, uint64_t* key, uint64_t* lo
 // glibc-exact math restatement, for the CPU bit-compare test.
 void hostsim_math(int fn, const double* x, const double* y, double* out, long n) {
     for (long i = 0; i < n; ++i)
-        out[i] = fn == 0 ? mg::gl_log(x[i]) : fn == 1 ? mg::gl_exp(x[i]) : mg::gl_pow(x[i], y[i]);
+        out[i] = fn == 0 ? mg::gl_log(x[i]) : fn == 1 ? mg::gl_exp(x[i]) : fn == 2 ? mg::gl_pow(x[i], y[i])
+                                                                 : mg::fmod_fast(x[i], y[i]);
 }
 
 // the engine's sliding window (des_core.h TailWin: cached top-K + linear selection beyond it):

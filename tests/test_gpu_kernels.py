@@ -36,6 +36,22 @@ def test_device_libm_bit_exact(engine, fn):
     assert same.all(), (xs[~same][:4], o[~same][:4], ref[~same][:4])
 
 
+def test_device_fmod_fast_exact(engine):
+    """the event loop's schedule phase (fmod_fast, arrivals.h sched_active) vs C fmod, on the device"""
+    from tests.test_host_logic import _fmod_inputs
+
+    x, y = _fmod_inputs(400000, np.random.default_rng(12))
+    out = np.zeros_like(x)
+    lib = engine._lib
+    lib.migsim_gpu_libm.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]
+    err = ctypes.create_string_buffer(512)
+    assert lib.migsim_gpu_libm(engine._h, 3, x.ctypes.data, y.ctypes.data, out.ctypes.data, len(x), err, 512) == 0
+    ref = np.fmod(x, y)
+    same = (out.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(out) & np.isnan(ref))
+    assert same.all(), (x[~same][:5], y[~same][:5], out[~same][:5], ref[~same][:5])
+
+
 @pytest.mark.parametrize("path", GOLDEN_SCENARIOS + CONFIG_SCENARIOS)
 def test_device_arrivals_bit_exact(engine, path):
     lib = engine._lib

@@ -306,3 +306,28 @@ def test_select_jth_largest_is_the_sorted_order_statistic():
         s = np.sort(v)[::-1]
         for j in {0, n // 3, n - 1}:
             assert lib.hostsim_select_jth(v.ctypes.data, n, j) == s[j]
+
+
+def _fmod_inputs(n, rng):
+    """schedule phases (t - offset over [0, 1800] s, periods 1..600 s) plus wide and edge cases"""
+    t = rng.uniform(-700.0, 4000.0, n)
+    p = rng.choice([60.0, 120.0, 0.1, 7.5, 1.0 / 3.0, 600.0], n) * rng.choice([1.0, 1.0 + 1e-12], n)
+    wide_x = rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n)
+    wide_y = np.abs(rng.standard_normal(n)) * 10.0 ** rng.integers(-300, 300, n)
+    k = rng.integers(0, 1 << 19, n).astype(np.float64)
+    multiples = k * p  # exact and near-exact multiples: remainders 0 / tiny / y - tiny
+    x = np.concatenate([t, wide_x, multiples, np.nextafter(multiples, np.inf), np.nextafter(multiples, -np.inf),
+                        [0.0, -0.0, 5.0, -5.0, np.inf, np.nan, 1e-320, 7.0, 1e300]])
+    y = np.concatenate([p, wide_y, p, p, p, [3.0, 3.0, 0.0, -3.0, 2.0, 2.0, 3.0, 1e-310, 1e-300]])
+    return np.ascontiguousarray(x), np.ascontiguousarray(y)
+
+
+def test_fmod_fast_exact():
+    """glibc_math.h fmod_fast (schedule phase) vs C fmod: exact on every input (fast path + fallback)."""
+    rng = np.random.default_rng(11)
+    x, y = _fmod_inputs(200000, rng)
+    out = np.zeros_like(x)
+    hostsim().hostsim_math(3, x.ctypes.data, y.ctypes.data, out.ctypes.data, len(x))
+    ref = np.fmod(x, y)
+    same = (out.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(out) & np.isnan(ref))
+    assert same.all(), (x[~same][:5], y[~same][:5], out[~same][:5], ref[~same][:5])

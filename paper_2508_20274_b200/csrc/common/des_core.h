@@ -269,6 +269,7 @@ struct TenantDyn {
     int32_t n_count, root;  // root: canonical PCIe root of the current placement
     double frac;    // sm_fraction of the current (gpu, profile) (engine.cpp:330-334)
     double cap_eff; // effective_pcie_cap_Bps of the current throttle state (model.cpp:155-159)
+    double obs_lat, obs_arrived;  // the completion handed to the deferred controller step (kOpObserve)
 };
 
 MG_HD int __popcll_hd(uint64_t m) {
@@ -392,6 +393,17 @@ struct Sim {
     double measure_start;
     int n_irq, redistribute;
     Mask live_resume, live_expire;  // tenants with a live resume / guardrail-expire event
+    // Continuation ops (warp-uniform registers).  The hot handlers do not inline the shared
+    // pipeline helpers at each call site; they queue them, and the event loop runs every queued op
+    // from ONE copy of each helper (run_ops), so the event loop's instruction working set holds one
+    // reallocate_root / start_compute / start_transfer instead of 3 / 2 / 2 inlined copies (the
+    // saturated-regime DES is instruction-fetch bound).  An op is
+    // (code << 7 | arg) in a 10-bit field; `ops` runs front (low bits) first; ops queued while an
+    // op runs go to `cont` and run before the rest of `ops`, so the order of every state change and
+    // push is exactly the nested-call order of the reference.  At most 3 ops are ever pending (a
+    // transfer completion queues 3; only the last of them, a start_transfer, queues more, <= 2).
+    uint32_t ops, cont;
+    int n_cont;
     // Working-set arrays held as registers (not re-loaded from SimState) so that, after inlining
     // into the kernel, the compiler sees shared-memory provenance and emits LDS/STS.
     TenantDyn* td;
@@ -407,7 +419,7 @@ struct Sim {
     MG_HD Sim(const PScenario& s, const PController& c, const ReplicaIO& i, SimState& state, Lanes l,
               TenantDyn* tdp, TenantCtl* ctlp, RootDyn* rdp)
         : S(s), C(c), io(i), st(state), lanes(l), T(s.n_tenants), now(0.0), next_seq(0), n_events(0),
-          live_resume(0), live_expire(0), measure_start(s.measure_start_s), n_irq(s.n_irq),
+          live_resume(0), live_expire(0), ops(0), cont(0), n_cont(0), measure_start(s.measure_start_s), n_irq(s.n_irq),
           redistribute(s.fabric_redistribute), td(tdp), ctl(ctlp), rd(rdp), tn(s.tenants), gp(s.gpus), rt(s.roots),
           iq(s.irq), hio(s.host_io_capacity) {}
 
@@ -645,7 +657,9 @@ struct Sim {
         push(kEvCompute, i, d.compute_end);
     }
 
-    MG_HOT void start_transfer(int i) {
+    // kDefer: the tail calls are queued as continuation ops (hot callers); otherwise run in place
+    template <bool kDefer>
+    MG_HD void start_transfer_t(int i) {
         TenantDyn& d = td[i];
         if (d.transferring || d.paused) return;
         const int64_t base = d.base;
@@ -654,6 +668,11 @@ struct Sim {
             const double bytes = io.arr_bytes[base + k];
             if (bytes <= 0.0) {
                 io.req_transfer_ms[base + k] = 0.0;
+                if (kDefer) {  // start_compute, then this loop again (re-entry sees the same flags)
+                    then(kOpStartCompute, i);
+                    then(kOpStartTransfer, i);
+                    return;
+                }
                 start_compute(i);
                 continue;
             }
@@ -664,8 +683,45 @@ struct Sim {
             const int r = root_of(i);
             settle_root(r);
             rd[r].active |= 1ull << i;
-            reallocate_root(r);
+            if (kDefer) then(kOpRealloc, r);
+            else reallocate_root(r);
             return;
+        }
+    }
+    MG_HOT void start_transfer(int i) { start_transfer_t<false>(i); }
+
+    // ---- continuation ops ----------------------------------------------------------------
+    enum : uint32_t { kOpRealloc = 1, kOpStartCompute = 2, kOpStartTransfer = 3, kOpObserve = 4 };
+    MG_HD void then(uint32_t code, int arg) {  // arg: a tenant (< 64) or root (< 16) index
+        cont |= ((code << 7) | static_cast<uint32_t>(arg)) << (10 * n_cont);
+        n_cont += 1;
+    }
+    // the deferred controller step of a completion (engine.cpp:497-503: on_observation, then the
+    // returned action is applied)
+    MG_HD void observe(int i) {
+        const TenantDyn& d = td[i];
+        Action a = on_observation(i, d.obs_lat, now, d.obs_arrived);
+        if (a.valid) apply_action(a);
+    }
+    // run the ops the handler queued, depth first (if-chain in frequency order: no indirect branch)
+    MG_HD void run_ops() {
+        ops = cont;
+        cont = 0;
+        n_cont = 0;
+        while (ops) {
+            const uint32_t code = (ops >> 7) & 7u;
+            const int arg = static_cast<int>(ops & 0x7fu);
+            ops >>= 10;
+            if (code == kOpRealloc) reallocate_root(arg);
+            else if (code == kOpStartCompute) start_compute(arg);
+            else if (code == kOpStartTransfer) start_transfer_t<true>(arg);
+            else observe(arg);
+            if (n_cont) {
+                if (n_cont > 3 || (ops >> (30 - 10 * n_cont)) != 0) st.error = kErrOpOverflow;
+                ops = cont | (ops << (10 * n_cont));
+                cont = 0;
+                n_cont = 0;
+            }
         }
     }
 
@@ -676,8 +732,10 @@ struct Sim {
         // (no software prefetch of the arrival records: an L1 prefetch per 16 records measured 2%
         //  slower than letting the in-order loads miss)
         d.n_arrived = k + 1;
-        start_transfer(i);
+        // start_transfer is deferred past the next-arrival push: only same-kind pushes compare by
+        // seq, and their relative order is unchanged
         if (d.n_arrived < d.n_count) push(kEvArrival, i, io.arr_t[d.base + d.n_arrived]);
+        then(kOpStartTransfer, i);
     }
 
     MG_HD void on_transfer_complete(int i) {
@@ -688,7 +746,7 @@ struct Sim {
         const bool done =
             rem <= kEpsBytes || (d.grant > 0.0 && fadd(now, fdiv_exact(rem, d.grant)) <= now);
         if (!done) {
-            reallocate_root(r);
+            then(kOpRealloc, r);
             return;
         }
         d.remaining = 0.0;
@@ -697,9 +755,9 @@ struct Sim {
         io.req_transfer_ms[d.base + k] = fadd(d.transfer_ms, fmul(fsub(now, d.started_s), 1000.0));
         rd[r].active &= ~(1ull << i);
         d.grant = 0.0;
-        reallocate_root(r);
-        start_compute(i);
-        start_transfer(i);
+        then(kOpRealloc, r);
+        then(kOpStartCompute, i);
+        then(kOpStartTransfer, i);
     }
 
     MG_HD void on_compute_complete(int i) {
@@ -737,10 +795,11 @@ struct Sim {
         }
         st.done_seq += 1;
         if (io.tr_win) tw_push(io.tr_win[i], total);
-        start_compute(i);
+        then(kOpStartCompute, i);
         if (C.enabled) {
-            Action a = on_observation(i, total, now, arrived);
-            if (a.valid) apply_action(a);
+            d.obs_lat = total;
+            d.obs_arrived = arrived;
+            then(kOpObserve, i);
         }
     }
 
@@ -1494,6 +1553,7 @@ struct Sim {
             d.started_s = -1.0;
             d.compute_done_ms = d.svc_ms = d.extra_ms = d.compute_end = d.cur_transfer_ms = 0.0;
             d.pend_pause = 0.0;
+            d.obs_lat = d.obs_arrived = 0.0;
             d.completed = d.n_window = d.misses = d.pad_c = 0;
             d.sum_total = 0.0;
             d.win_min = k_inf();
@@ -1542,6 +1602,7 @@ struct Sim {
             case kEvArrival: on_arrival(i); break;
             default: on_tick(); break;
         }
+        run_ops();
     }
 
     // host event loop (engine.cpp:864-894); the device loop lives in des_kernel

@@ -68,6 +68,7 @@ enum : int32_t {
     kErrPauseOverflow = 2,
     kErrArrivalOverflow = 3,
     kErrSeqOverflow = 4,  // > 2^29 event pushes in one replica
+    kErrOpOverflow = 5,   // continuation-op word overflow (des_core.h run_ops; structurally impossible)
 };
 
 struct ReplicaOut {

@@ -69,7 +69,8 @@ typedef struct migsim_timing {
     double gen_ms, des_ms, select_ms, total_device_ms, wall_ms;
     int64_t replicas, tenant_ticks, completions, arrivals, events, waves;
     int64_t select_samples;  /* measurement-window latencies fed to the select kernel */
-    int64_t des_simt;        /* 1: the SIMT DES ran (one thread per replica), 0: warp per replica */
+    int64_t des_form;        /* DES kernel: 0 warp per replica, 1 SIMT (thread per replica),
+                                2 warp per replica register-capped (saturated batches) */
     int64_t des_blocks_per_sm; /* occupancy of the DES launch (resident blocks per SM) */
     int64_t des_smem_bytes;    /* dynamic shared memory per DES block */
     int64_t kernel_launches;   /* engine kernels launched by the call */

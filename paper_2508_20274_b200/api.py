@@ -70,7 +70,7 @@ class _Timing(ctypes.Structure):
         ("events", ctypes.c_int64),
         ("waves", ctypes.c_int64),
         ("select_samples", ctypes.c_int64),
-        ("des_simt", ctypes.c_int64),
+        ("des_form", ctypes.c_int64),
         ("des_blocks_per_sm", ctypes.c_int64),
         ("des_smem_bytes", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64),

@@ -305,9 +305,17 @@ MG_HD void prefetch_l1(const void* p) {
 #endif
 }
 
+// Grant cache of a root: the bandwidth split of reallocate_root (PS shares + water-filling,
+// fabric.cpp:31-87) is a pure function of the active flow set, given the root capacity, the flow
+// weights and the tenants' effective PCIe caps; the caps change only in Sim::refresh, which empties
+// every cache.  Replaying a cached split writes the identical doubles.  Direct-mapped on the mask.
+constexpr int kGcEntries = 4, kGcFlows = 4;
 struct RootDyn {
     uint64_t active;  // tenant bitmask, iteration in id order == sorted root.active
+    uint64_t gc_mask[kGcEntries];           // cached active sets (0 = empty entry)
+    double gc_grant[kGcEntries][kGcFlows];  // their grants, members in id order
 };
+MG_HD int gc_entry(uint64_t m) { return static_cast<int>((m ^ (m >> 2) ^ (m >> 5) ^ (m >> 11)) & (kGcEntries - 1)); }
 
 struct Slot {
     double t;
@@ -434,6 +442,8 @@ struct Sim {
         d.frac = calc_frac(i);
         const double base = spec(i).pcie_cap;
         d.cap_eff = !d.has_throttle ? base : base > 0.0 ? (d.io_throttle < base ? d.io_throttle : base) : d.io_throttle;
+        for (int r = 0; r < S.n_roots; ++r)
+            for (int e = 0; e < kGcEntries; ++e) rd[r].gc_mask[e] = 0;
     }
     // Slot layout: the three per-request kinds first, then the tick, then the rare kinds, so the
     // device argmin scans only 3T+1 slots while no resume/expire event is live (any_rare() false).
@@ -544,7 +554,12 @@ struct Sim {
     MG_HOT void reallocate_root(int r) {
         const Mask act = static_cast<Mask>(rd[r].active);
         const double cap = rt[r].capacity;
-        if (act) {
+        const int ge = gc_entry(act);
+        const bool cacheable = __popcll_hd(act) <= kGcFlows;
+        if (act && cacheable && rd[r].gc_mask[ge] == act) {
+            int k = 0;
+            for (Mask m = act; m; m &= m - 1) td[ctz64(m)].grant = rd[r].gc_grant[ge][k++];
+        } else if (act) {
             double wsum = 0.0;
             for (Mask m = act; m; m &= m - 1) wsum = fadd(wsum, spec(ctz64(m)).weight);
             double granted = 0.0;
@@ -583,6 +598,11 @@ struct Sim {
                     residual = fsub(residual, moved);
                     if (moved <= fmul(1e-12, cap)) break;
                 }
+            }
+            if (cacheable) {
+                int k = 0;
+                for (Mask m = act; m; m &= m - 1) rd[r].gc_grant[ge][k++] = td[ctz64(m)].grant;
+                rd[r].gc_mask[ge] = act;
             }
         }
         for (Mask m = act; m; m &= m - 1) {
@@ -1528,6 +1548,7 @@ struct Sim {
         st.done_seq = 0;
         for (int r = 0; r < S.n_roots; ++r) {
             rd[r].active = 0;
+            for (int e = 0; e < kGcEntries; ++e) rd[r].gc_mask[e] = 0;
             io.backlog[2 * r] = 0.0;
             io.backlog[2 * r + 1] = 0.0;
         }

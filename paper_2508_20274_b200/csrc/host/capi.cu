@@ -241,6 +241,20 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     }
     if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false, G, I, H);
     auto* des = T <= mg::kRegSlotMaxTenants ? mg::des_kernel_reg : mg::des_kernel;
+    // register-capped form when the batch saturates the uncapped kernel's resident slots
+    // (MIGSIM_DES_REGS=full|capped overrides)
+    bool des_capped = false;
+    if (!use_simt && T <= mg::kRegSlotMaxTenants) {
+        const char* regs_env = std::getenv("MIGSIM_DES_REGS");
+        const std::string regs_mode = regs_env ? regs_env : "auto";
+        int occ_full = 0, nsm = 0;
+        CK(cudaFuncSetAttribute(mg::des_kernel_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(L.total)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_full, mg::des_kernel_reg, 32, static_cast<size_t>(L.total)));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device));
+        des_capped = regs_mode == "capped" ||
+                     (regs_mode == "auto" && n_jobs > static_cast<size_t>(occ_full) * static_cast<size_t>(nsm));
+        if (des_capped) des = mg::des_kernel_reg_occ;
+    }
     if (use_simt)
         CK(cudaFuncSetAttribute(mg::des_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(Y.bytes(simt_lanes))));
@@ -715,7 +729,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     res.timing.events = events;
     res.timing.waves = waves;
     res.timing.select_samples = samples;
-    res.timing.des_simt = use_simt ? 1 : 0;
+    res.timing.des_form = use_simt ? 1 : des_capped ? 2 : 0;
     res.timing.des_blocks_per_sm = des_blocks_per_sm;
     res.timing.des_smem_bytes = use_simt ? Y.bytes(simt_lanes) : L.total;
     res.timing.kernel_launches = launches;

@@ -59,6 +59,10 @@ __global__ void des_kernel(const PScenario* __restrict__ S, const PController* _
 constexpr int kRegSlotMaxTenants = 10;  // 3T+1 hot slots and 2T rare slots within 32 lanes
 __global__ void des_kernel_reg(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
                                int n_rep, SimLayout L);
+// same code capped at 64 registers (32 resident warps/SM instead of 16): the saturated-regime form,
+// used when a wave holds more replicas than the uncapped kernel keeps resident
+__global__ void des_kernel_reg_occ(const PScenario* __restrict__ S, const PController* __restrict__ C, WaveBuffers B,
+                                   int n_rep, SimLayout L);
 // SIMT form: one thread per replica, for large waves (see engine_kernels.cu)
 constexpr int kSimtMaxTenants = 32;  // 32-bit tenant masks
 constexpr int kSimtBlock = 32;       // threads (replicas) per block, at most

@@ -76,7 +76,7 @@ def test_simt_equals_warp_form(engine, monkeypatch):
     for mode in ("warp", "simt"):
         monkeypatch.setenv("MIGSIM_DES", mode)
         res = engine.run_batch(sid, list(range(1, 129)), vs)
-        assert res.timing["des_simt"] == (mode == "simt")
+        assert (res.timing["des_form"] == 1) == (mode == "simt")
         outs[mode] = (res.rows.copy(), [res.run(k)["actions"] for k in range(0, res.n_runs, 7)])
         res.close()
     assert (outs["warp"][0].view(np.uint8) == outs["simt"][0].view(np.uint8)).all()

@@ -37,7 +37,7 @@ for mode in modes:
         res.close()
     out[mode] = (rows, sample)
     tt = best["tenant_ticks"] / (best["total_device_ms"] / 1e3)
-    print(json.dumps({"mode": mode, "simt": int(best["des_simt"]), "replicas": int(best["replicas"]),
+    print(json.dumps({"mode": mode, "form": int(best["des_form"]), "regs": os.environ.get("MIGSIM_DES_REGS", "auto"), "replicas": int(best["replicas"]),
                       "waves": int(best["waves"]), "blocks_per_sm": int(best["des_blocks_per_sm"]),
                       "smem": int(best["des_smem_bytes"]), "lib": os.environ.get("MIGSIM_LIB", "default"),
                       "rings": os.environ.get("MIGSIM_RINGS", "auto"), "gen_ms": round(best["gen_ms"], 1), "des_ms": round(best["des_ms"], 1),

@@ -271,7 +271,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     const size_t resident = static_cast<size_t>(std::max(1, des_blocks_per_sm)) * static_cast<size_t>(n_sm) *
                             static_cast<size_t>(use_simt ? simt_lanes : 1);
     // wave size from free memory
-    const size_t per_rep = static_cast<size_t>(P.cap_sum) * 8 * (8 + (keep ? 5 : 0)) + static_cast<size_t>(T) * 8 +
+    // record streams per arrival slot: t, bytes, mult, noise, req_ms, win_lat (+ irq draws when some
+    // IRQ burst adds noise, + the unthinned clock when some tenant is schedule-thinned, + 5 with
+    // keep_completions)
+    const int n_streams = 6 + (P.any_irq_noise ? 1 : 0) + (P.any_thinned ? 1 : 0) + (keep ? 5 : 0);
+    const size_t per_rep = static_cast<size_t>(P.cap_sum) * 8 * static_cast<size_t>(n_streams) + static_cast<size_t>(T) * 8 +
                            static_cast<size_t>(T) * mg::kMtN * 8 + static_cast<size_t>(action_cap) * sizeof(mg::ActionRec) * 2 +
                            static_cast<size_t>(pause_cap) * sizeof(mg::PauseRec) * 2 + T * sizeof(mg::TenantOut) +
                            sizeof(mg::ReplicaOut) + static_cast<size_t>(R) * 16 + static_cast<size_t>(T) * 32 + 64 +
@@ -311,8 +315,12 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         S.arr_bytes.alloc(big);
         S.arr_mult.alloc(big);
         S.arr_noise.alloc(big);
-        S.irq_e.alloc(big);
-        S.t_all.alloc(big);
+        // (optional streams not needed by this batch are released: the wave sizing above counts
+        //  every cached buffer of the handle as reusable)
+        if (P.any_irq_noise) S.irq_e.alloc(big);
+        else S.irq_e.free();
+        if (P.any_thinned) S.t_all.alloc(big);
+        else S.t_all.free();
         S.req_ms.alloc(big);
         S.win_lat.alloc(big);
         S.win_hist.alloc(W * T * mg::kHistBins);
@@ -430,8 +438,8 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         B.arr_bytes = S.arr_bytes.p;
         B.arr_mult = S.arr_mult.p;
         B.arr_noise = S.arr_noise.p;
-        B.irq_e = S.irq_e.p;
-        B.t_all = S.t_all.p;
+        B.irq_e = P.any_irq_noise ? S.irq_e.p : nullptr;
+        B.t_all = P.any_thinned ? S.t_all.p : nullptr;
         B.req_ms = S.req_ms.p;
         B.win_lat = S.win_lat.p;
         B.win_hist = S.win_hist.p;

@@ -207,6 +207,7 @@ Packed pack(const ScenarioSpec& spec, const std::vector<Variant>& variants, doub
         o.has_noise = t.noise_mean_ms > 0.0;
         o.noise_lambda = o.has_noise ? 1.0 / t.noise_mean_ms : 0.0;
         pack_schedule(e.schedule, o.sched);
+        if (o.sched.kind != mg::kAlways) P.any_thinned = true;
         // record capacity: mean count + cap_sigmas standard deviations of a renewal count
         const double mean = t.arrival_rate_hz * spec.duration_s;
         const double cvx = std::max(cv, 0.5);

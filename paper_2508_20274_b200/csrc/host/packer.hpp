@@ -47,6 +47,7 @@ struct Packed {
     int64_t cap_sum = 0;
     int max_dwell = 0, max_validation = 0;
     bool any_irq_noise = false;
+    bool any_thinned = false;  // some tenant's arrivals are schedule-thinned (needs the unthinned clock)
 };
 
 // Throws ConfigError when the scenario exceeds the device representation limits.

@@ -22,7 +22,7 @@ __global__ void __launch_bounds__(32) gen_times_kernel(const PScenario* __restri
     int32_t* n_all = B.n_all + r * T + t;
     int32_t* n_kept = B.n_kept + r * T + t;
     const bool ok = warp_gen_times(g, p, substream_seed(B.seeds[r], p.name_hash, kArrivals), S->duration_s,
-                                   B.t_all + base, B.arr_t + base, B.cap[t], n_all, n_kept, lane);
+                                   B.t_all ? B.t_all + base : nullptr, B.arr_t + base, B.cap[t], n_all, n_kept, lane);
     if (!ok && lane == 0) atomicExch(B.gen_overflow, 1);
 }
 
@@ -43,12 +43,13 @@ __global__ void __launch_bounds__(32) gen_marks_kernel(const PScenario* __restri
     if (purpose == kMarkIrq) {
         if (!B.any_irq_noise) return;
         warp_gen_marks(mt, kMarkIrq, p, substream_seed(B.seeds[r], p.name_hash, kIrq), nullptr,
-                       B.n_kept[r * T + t], false, B.irq_e + base, lane);
+                       B.n_kept[r * T + t], false, B.irq_e ? B.irq_e + base : nullptr, lane);
         return;
     }
     const uint64_t sp = purpose == kMarkSize ? kTransferSize : purpose == kMarkService ? kService : kNoise;
     double* out = purpose == kMarkSize ? B.arr_bytes : purpose == kMarkService ? B.arr_mult : B.arr_noise;
-    warp_gen_marks(mt, purpose, p, substream_seed(B.seeds[r], p.name_hash, sp), B.t_all + base, B.n_all[r * T + t],
+    warp_gen_marks(mt, purpose, p, substream_seed(B.seeds[r], p.name_hash, sp), B.t_all ? B.t_all + base : nullptr,
+                   B.n_all[r * T + t],
                    p.sched.kind != kAlways, out + base, lane);
 }
 
@@ -218,7 +219,7 @@ __device__ __forceinline__ ReplicaIO replica_io(const WaveBuffers& B, const PSce
     io.arr_bytes = B.arr_bytes + base;
     io.arr_mult = B.arr_mult + base;
     io.arr_noise = B.arr_noise + base;
-    io.irq_e = B.irq_e + base;
+    io.irq_e = B.irq_e ? B.irq_e + base : nullptr;
     io.off = B.off;
     io.count = B.n_kept + static_cast<int64_t>(r) * T;
     io.seed = B.seeds[r];

@@ -21,7 +21,9 @@
 
 namespace mg {
 
-constexpr int kRing = 1024;       // canonical ring (positions)
+// canonical ring (positions): one 312-word block is written per fill, so the scan may look ahead
+// kRing - kMtN positions; 512 keeps the block's shared memory at ~17 KB (12 resident warps/SM)
+constexpr int kRing = 512;
 static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
 // ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
 __device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
@@ -212,7 +214,8 @@ __device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaP
                 cached = true;
                 p += 2;
             }
-            n = fadd(fmul(n, 1.0), 0.0);
+            // (libstdc++'s n*1.0+0.0 scaling is omitted: it only maps -0.0 to +0.0, and n enters
+            //  only as 1 + a2*n and through even powers)
             v = fadd(1.0, fmul(gp.a2, n));
         } while (v <= 0.0);
         v = fmul(fmul(v, v), v);
@@ -257,8 +260,13 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                     ok = false;
                     break;
                 }
-                t_all[na++] = clock;
-                if (!thinned || sched_active(p.sched, clock)) t_kept[nk++] = clock;
+                if (thinned) {
+                    t_all[na] = clock;
+                    if (sched_active(p.sched, clock)) t_kept[nk++] = clock;
+                } else {
+                    t_kept[nk++] = clock;
+                }
+                ++na;
             }
             *n_all_out = static_cast<int32_t>(na);
             *n_kept_out = static_cast<int32_t>(nk);
@@ -273,8 +281,8 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
     gen_end += kMtN;
     bool done = false;
     while (!done) {
-        // keep at least one full block of lookahead past the scan position
-        while (gen_end - pos < 2 * kMtN) {
+        // fill while the ring has room for a whole block without overwriting positions >= pos - 1
+        while (gen_end - pos < kRing - kMtN) {
             gamma_fill(g, gen_end, lane);
             gen_end += kMtN;
         }
@@ -317,8 +325,14 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                     done = true;
                     break;
                 }
-                t_all[na++] = clock;
-                if (!thinned || sched_active(p.sched, clock)) t_kept[nk++] = clock;
+                // the unthinned clock is read back only for thinned tenants (gen_marks)
+                if (thinned) {
+                    t_all[na] = clock;
+                    if (sched_active(p.sched, clock)) t_kept[nk++] = clock;
+                } else {
+                    t_kept[nk++] = clock;
+                }
+                ++na;
             }
         }
         done = __shfl_sync(0xffffffffu, done, 0);

@@ -357,7 +357,10 @@ __global__ void MG_DES_BOUNDS des_kernel_reg(const PScenario* __restrict__ S,
 // dependent-latency stalls dominate and twice the resident warps hide them (C4 wave: 780 -> 676 ms
 // at 64 vs 124 registers, no spills).  A latency-bound batch (fewer replicas than resident slots,
 // e.g. C2's 256) keeps the uncapped kernel, whose per-replica event chain is shorter.
-__global__ void __maxnreg__(64) des_kernel_reg_occ(const PScenario* __restrict__ S, const PController* __restrict__ C,
+#ifndef MG_OCC_MAXNREG
+#define MG_OCC_MAXNREG 64  // 48 / 56 measured slower: spills, and 1-warp blocks cap residency at 32/SM anyway
+#endif
+__global__ void __maxnreg__(MG_OCC_MAXNREG) des_kernel_reg_occ(const PScenario* __restrict__ S, const PController* __restrict__ C,
                                                    WaveBuffers B, int n_rep, SimLayout L) {
     des_body<RegLanes>(S, C, B, n_rep, L);
 }

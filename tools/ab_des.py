@@ -41,7 +41,7 @@ for mode in modes:
                       "waves": int(best["waves"]), "blocks_per_sm": int(best["des_blocks_per_sm"]),
                       "smem": int(best["des_smem_bytes"]), "lib": os.environ.get("MIGSIM_LIB", "default"),
                       "rings": os.environ.get("MIGSIM_RINGS", "auto"), "gen_ms": round(best["gen_ms"], 1), "des_ms": round(best["des_ms"], 1),
-                      "select_ms": round(best["select_ms"], 2), "tenant_ticks_per_s": tt,
+                      "select_ms": round(best["select_ms"], 2), "completions": int(best["completions"]), "tenant_ticks_per_s": tt,
                       "events_per_s": best["events"] / (best["des_ms"] / 1e3)}), flush=True)
 if len(out) > 1:
     ms = list(out)

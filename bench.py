@@ -307,9 +307,13 @@ def run_engine(args):
     if os.path.exists(tr_path):
         with open(tr_path) as f:
             tj = json.load(f)
-        traffic = {"dram_bytes_per_launch": tj.get("dram_bytes_per_launch"),
-                   "algorithmic_bytes_per_launch": tj.get("algorithmic_bytes_per_launch"),
-                   "source": tj.get("source")}
+        # ncu per-launch DRAM bytes of the captured launch, and its ratio to the algorithmic 48 B per
+        # completion applied to this run's DES launches (one launch per wave)
+        ratio = tj["dram_bytes_per_launch"] / tj["algorithmic_bytes_per_launch"]
+        alg_launch = 48.0 * acc["completions"] / max(1, acc["waves"])
+        traffic = {"dram_bytes_per_launch": ratio * alg_launch, "algorithmic_bytes_per_launch": alg_launch,
+                   "dram_over_algorithmic": ratio, "captured_kernel": tj.get("kernel"),
+                   "captured_workload": tj.get("workload"), "source": tj.get("source")}
     value = acc["tenant_ticks"] / (dev_ms / 1000.0)
     sec = None
     if args.c2_seeds > 0:
@@ -344,7 +348,8 @@ def run_engine(args):
                 "note": "wall clock around the C-ABI call (host packing, H2D, kernels, D2H of every RunResult) "
                         "+ the cross-rank reduction, max over ranks"},
         "gpu_launches": int(acc["kernel_launches"]),
-        "roofline": {"bound": "hbm", "kernel": "des_kernel_reg" if T <= 10 else "des_kernel", "achieved": des_gbs,
+        "roofline": {"bound": "hbm", "kernel": {0: "des_kernel_reg" if T <= 10 else "des_kernel", 1: "des_simt_kernel",
+                                                2: "des_kernel_reg_occ"}[int(t_last["des_form"])], "achieved": des_gbs,
                      "peak": hbm, "unit": "GB/s", "frac": des_gbs / hbm, "traffic": traffic, "peak_kind": peak_kind,
                      "note": "replica DES is latency/issue bound (one sequential event loop per warp); "
                              "48 B algorithmic per completion"},

@@ -27,7 +27,7 @@ constexpr int kRing = 512;
 static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
 // ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
 __device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
-constexpr int kMaxCallsRound = 160;
+constexpr int kMaxCallsRound = 128;  // gamma calls scanned per round (~150 fit the 200-position lookahead)
 
 struct WarpMtSmem {
     uint64_t x[kMtN];
@@ -162,9 +162,8 @@ struct GammaSmem {
     double ny[kRing];   // y*mult if the pair starting at p is accepted
     double nx[kRing];   // x*mult (the polar cache)
     uint8_t acc[kRing];
-    double call_v[kMaxCallsRound];
+    double call_v[kMaxCallsRound];  // the call's v, then (in place) its gap value
     int32_t call_q[kMaxCallsRound];
-    double call_g[kMaxCallsRound];
     int32_t n_calls;
 };
 
@@ -308,14 +307,14 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         // lane-parallel gap values: pow(u, 1/alpha) * a1 * v * beta (random.tcc:2382-2392)
         for (int k = lane; k < nc; k += 32) {
             const double v = g.call_v[k];
-            if (g.call_q[k] < 0) g.call_g[k] = fmul(fmul(gp.a1, v), gp.beta);
-            else g.call_g[k] = fmul(fmul(fmul(gl_pow(g.c[g.call_q[k]], gp.inv_alpha), gp.a1), v), gp.beta);
+            if (g.call_q[k] < 0) g.call_v[k] = fmul(fmul(gp.a1, v), gp.beta);
+            else g.call_v[k] = fmul(fmul(fmul(gl_pow(g.c[g.call_q[k]], gp.inv_alpha), gp.a1), v), gp.beta);
         }
         __syncwarp();
         // lane 0: the clock is an ordered FP sum (workload.cpp:135)
         if (lane == 0) {
             for (int32_t k = 0; k < nc; ++k) {
-                clock = fadd(clock, g.call_g[k]);
+                clock = fadd(clock, g.call_v[k]);
                 if (clock >= duration) {
                     done = true;
                     break;

@@ -342,19 +342,27 @@ struct SimLayout {
     int64_t sc_tn, sc_gp, sc_rt, sc_iq, sc_hio, sc_ctrl, st;
 };
 MG_HD int64_t align16(int64_t x) { return (x + 15) & ~static_cast<int64_t>(15); }
-MG_HD SimLayout sim_layout(int T, int R, int W, int V, bool rings, int G = 0, int I = 0, int H = 0) {
+// global_tables: the read-only scenario tables stay in global memory (read through L1 by every
+// replica of the SM; sc_* = -1) and only the PController is staged -- for the T > 10 kernel, where a
+// per-replica copy of 64 PTenant rows (30 KB) caps the DES at 3 replicas per SM.
+MG_HD SimLayout sim_layout(int T, int R, int W, int V, bool rings, int G = 0, int I = 0, int H = 0,
+                           bool global_tables = false) {
     SimLayout L;
     int64_t o = 0;
-    L.sc_tn = o;
-    o = align16(o + static_cast<int64_t>(sizeof(PTenant)) * T);
-    L.sc_gp = o;
-    o = align16(o + static_cast<int64_t>(sizeof(PGpu)) * G);
-    L.sc_rt = o;
-    o = align16(o + static_cast<int64_t>(sizeof(PRoot)) * R);
-    L.sc_iq = o;
-    o = align16(o + static_cast<int64_t>(sizeof(PIrq)) * I);
-    L.sc_hio = o;
-    o = align16(o + 8ll * H);
+    if (global_tables) {
+        L.sc_tn = L.sc_gp = L.sc_rt = L.sc_iq = L.sc_hio = -1;
+    } else {
+        L.sc_tn = o;
+        o = align16(o + static_cast<int64_t>(sizeof(PTenant)) * T);
+        L.sc_gp = o;
+        o = align16(o + static_cast<int64_t>(sizeof(PGpu)) * G);
+        L.sc_rt = o;
+        o = align16(o + static_cast<int64_t>(sizeof(PRoot)) * R);
+        L.sc_iq = o;
+        o = align16(o + static_cast<int64_t>(sizeof(PIrq)) * I);
+        L.sc_hio = o;
+        o = align16(o + 8ll * H);
+    }
     L.sc_ctrl = o;
     o = align16(o + static_cast<int64_t>(sizeof(PController)));
     if (G == 0) o = 0;  // host harness: no copies

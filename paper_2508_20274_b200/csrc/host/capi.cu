@@ -213,7 +213,9 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     const bool keep = opts.keep_completions != 0 || traces;
     // working-set layout: controller rings in shared memory when a replica stays under 96 KB
     const int G = P.scen.n_gpus, I = P.scen.n_irq, H = P.scen.n_hosts;
-    mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true, G, I, H);
+    // T > 10 (des_kernel): scenario tables read from global memory, not staged per replica
+    const bool global_tables = T > mg::kRegSlotMaxTenants;
+    mg::SimLayout L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, true, G, I, H, global_tables);
     // DES form: SIMT (one thread per replica) for large batches, warp-per-replica otherwise
     // (MIGSIM_DES=warp|simt overrides)
     const mg::SimtLayout Y = mg::simt_layout(T, R, G, I, H, static_cast<int>(n_var));
@@ -239,7 +241,7 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
         CK(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, g->device));
         if (n_jobs > static_cast<size_t>(occ) * static_cast<size_t>(n_sm)) rings_in_smem = false;
     }
-    if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false, G, I, H);
+    if (!rings_in_smem) L = mg::sim_layout(T, R, P.max_dwell, P.max_validation, false, G, I, H, global_tables);
     auto* des = T <= mg::kRegSlotMaxTenants ? mg::des_kernel_reg : mg::des_kernel;
     // register-capped form when the batch saturates the uncapped kernel's resident slots
     // (MIGSIM_DES_REGS=full|capped overrides)

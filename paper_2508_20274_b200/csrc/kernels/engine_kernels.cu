@@ -257,7 +257,8 @@ __device__ __forceinline__ ReplicaIO replica_io(const WaveBuffers& B, const PSce
     return io;
 }
 
-template <class Lanes>
+// kGlobalTables: the scenario tables are read from global memory (layout sc_* = -1; T > 10 kernel)
+template <class Lanes, bool kGlobalTables = false>
 __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const PController* __restrict__ C,
                                          const WaveBuffers& B, int n_rep, const SimLayout& L) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -265,7 +266,7 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
     if (r >= n_rep) return;
     const int T = S->n_tenants;
     const int lane = threadIdx.x;
-    copy_tables(smem, L, S, lane, 32);
+    if (!kGlobalTables) copy_tables(smem, L, S, lane, 32);
     {
         const uint64_t* s8 = reinterpret_cast<const uint64_t*>(C + B.variant[r]);
         uint64_t* d8 = reinterpret_cast<uint64_t*>(smem + L.sc_ctrl);
@@ -288,11 +289,13 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
     }
     const ReplicaIO io = replica_io(B, S, r, T);
     Sim<Lanes> sim(*S, Cv, io, st, make_lanes<Lanes>(smem, L, T), td, ctl, rd);
-    sim.tn = reinterpret_cast<const PTenant*>(smem + L.sc_tn);
-    sim.gp = reinterpret_cast<const PGpu*>(smem + L.sc_gp);
-    sim.rt = reinterpret_cast<const PRoot*>(smem + L.sc_rt);
-    sim.iq = reinterpret_cast<const PIrq*>(smem + L.sc_iq);
-    sim.hio = reinterpret_cast<const double*>(smem + L.sc_hio);
+    if (!kGlobalTables) {
+        sim.tn = reinterpret_cast<const PTenant*>(smem + L.sc_tn);
+        sim.gp = reinterpret_cast<const PGpu*>(smem + L.sc_gp);
+        sim.rt = reinterpret_cast<const PRoot*>(smem + L.sc_rt);
+        sim.iq = reinterpret_cast<const PIrq*>(smem + L.sc_iq);
+        sim.hio = reinterpret_cast<const double*>(smem + L.sc_hio);
+    }  // else: the Sim constructor's S->tenants / gpus / roots / irq / host_io_capacity
     // The handlers run warp-uniformly: every lane executes the same instructions on the same
     // shared-memory words (broadcast loads, same-value stores), so no lane-0 divergence region
     // (BSSY/BSYNC) wraps the hot path.
@@ -340,7 +343,7 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
 
 __global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C,
                                                  WaveBuffers B, int n_rep, SimLayout L) {
-    des_body<HostLanes>(S, C, B, n_rep, L);
+    des_body<HostLanes, true>(S, C, B, n_rep, L);
 }
 
 #ifdef MG_DES_MAXNREG

@@ -341,7 +341,14 @@ __device__ __forceinline__ void des_body(const PScenario* __restrict__ S, const 
 #endif
 }
 
-__global__ void __launch_bounds__(32) des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C,
+// T > 10 kernel register budget: with __launch_bounds__(32) alone ptxas settles on 80 registers
+// and spills 404 B; 168 (148 used, no spills) measured -12% DES on C5 (occupancy is shared-memory
+// bound at 5 replicas/SM either way; profiles/r2_ab_c5_regs.txt)
+#ifndef MG_DESK_MAXNREG
+#define MG_DESK_MAXNREG 168
+#endif
+#define MG_DESK_BOUNDS __maxnreg__(MG_DESK_MAXNREG)
+__global__ void MG_DESK_BOUNDS des_kernel(const PScenario* __restrict__ S, const PController* __restrict__ C,
                                                  WaveBuffers B, int n_rep, SimLayout L) {
     des_body<HostLanes, true>(S, C, B, n_rep, L);
 }

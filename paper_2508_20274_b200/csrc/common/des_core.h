@@ -309,7 +309,10 @@ MG_HD void prefetch_l1(const void* p) {
 // fabric.cpp:31-87) is a pure function of the active flow set, given the root capacity, the flow
 // weights and the tenants' effective PCIe caps; the caps change only in Sim::refresh, which empties
 // every cache.  Replaying a cached split writes the identical doubles.  Direct-mapped on the mask.
-constexpr int kGcEntries = 4, kGcFlows = 4;
+#ifndef MG_GC_ENTRIES
+#define MG_GC_ENTRIES 4
+#endif
+constexpr int kGcEntries = MG_GC_ENTRIES, kGcFlows = 4;
 struct RootDyn {
     uint64_t active;  // tenant bitmask, iteration in id order == sorted root.active
     uint64_t gc_mask[kGcEntries];           // cached active sets (0 = empty entry)

@@ -27,7 +27,7 @@ constexpr int kRing = 512;
 static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
 // ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
 __device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
-constexpr int kMaxCallsRound = 128;  // gamma calls scanned per round (~150 fit the 200-position lookahead)
+constexpr int kMaxCallsRound = 80;  // gamma calls scanned per round (keeps the block at 15.6 KB: 14 warps/SM)
 
 struct WarpMtSmem {
     uint64_t x[kMtN];
@@ -159,11 +159,10 @@ __device__ void warp_gen_marks(WarpMtSmem& m, int purpose, const PTenant& p, uin
 struct GammaSmem {
     WarpMtSmem mt;
     double c[kRing];    // canonical at position p (ring)
-    double ny[kRing];   // y*mult if the pair starting at p is accepted
+    double ny[kRing];   // y*mult if the pair starting at p is accepted, NaN if it is rejected
     double nx[kRing];   // x*mult (the polar cache)
-    uint8_t acc[kRing];
     double call_v[kMaxCallsRound];  // the call's v, then (in place) its gap value
-    int32_t call_q[kMaxCallsRound];
+    int16_t call_q[kMaxCallsRound];  // ring index of the call's pow uniform, -1: none
     int32_t n_calls;
 };
 
@@ -180,11 +179,12 @@ __device__ __forceinline__ void gamma_fill(GammaSmem& g, int64_t gen_end, int la
         const double y = fsub(fmul(2.0, g.c[ring_idx(pos + 1)]), 1.0);
         const double r2 = fadd(fmul(x, x), fmul(y, y));
         const bool a = !(r2 > 1.0 || r2 == 0.0);
-        g.acc[ring_idx(pos)] = a;
         if (a) {
             const double mult = fsqrt(fdiv_exact(fmul(-2.0, gl_log(r2)), r2));
             g.ny[ring_idx(pos)] = fmul(y, mult);
             g.nx[ring_idx(pos)] = fmul(x, mult);
+        } else {
+            g.ny[ring_idx(pos)] = k_nan();  // an accepted pair's normals are finite
         }
     }
     __syncwarp();
@@ -205,10 +205,10 @@ __device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaP
             } else {
                 for (;;) {
                     if (p + 1 >= limit) return false;
-                    if (g.acc[ring_idx(p)]) break;
+                    n = g.ny[ring_idx(p)];
+                    if (n == n) break;  // accepted pair
                     p += 2;
                 }
-                n = g.ny[ring_idx(p)];
                 cache = g.nx[ring_idx(p)];
                 cached = true;
                 p += 2;
@@ -295,7 +295,7 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                 int32_t q;
                 if (!gamma_scan_call(g, gp, pp, limit, v, q)) break;
                 g.call_v[nc] = v;
-                g.call_q[nc] = q;
+                g.call_q[nc] = static_cast<int16_t>(q);
                 ++nc;
                 pos = pp;
             }

@@ -230,6 +230,9 @@ def run_engine(args):
         import torch.distributed as dist
 
         torch.cuda.set_device(device)
+        if n_dev < world:  # ranks share devices (test boxes): split each device's HBM between them
+            share = -(-world // max(n_dev, 1))
+            os.environ.setdefault("MIGSIM_MEM_FRACTION", str(0.70 / share))
         dist.init_process_group("nccl" if coll_dev == "cuda" else "gloo")
     from paper_2508_20274_b200 import Engine, Variant, sharding
 

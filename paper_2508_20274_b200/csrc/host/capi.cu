@@ -286,7 +286,11 @@ void run_batch_impl(migsim_gpu* g, const mgb::ScenarioSpec& spec, const std::vec
     size_t free_b = 0, total_b = 0;
     CK(cudaMemGetInfo(&free_b, &total_b));
     free_b += g->wave[0].bytes() + g->wave[1].bytes();  // the handle's cached wave buffers are reusable
-    size_t W = std::max<size_t>(1, static_cast<size_t>(0.70 * static_cast<double>(free_b)) / per_rep);
+    // MIGSIM_MEM_FRACTION: share of free HBM a batch's waves may use (default 0.70; processes that
+    // share one device, e.g. test launches of several ranks on one GPU, pass their share)
+    const char* frac_env = std::getenv("MIGSIM_MEM_FRACTION");
+    const double mem_frac = frac_env ? std::min(0.9, std::max(0.01, std::atof(frac_env))) : 0.70;
+    size_t W = std::max<size_t>(1, static_cast<size_t>(mem_frac * static_cast<double>(free_b)) / per_rep);
     if (opts.max_wave_replicas > 0) W = std::min<size_t>(W, static_cast<size_t>(opts.max_wave_replicas));
     // A multi-wave batch wastes the last, partly filled round of every wave (the event loop of a
     // wave ends with its slowest resident replicas).  Round the wave down to whole rounds of

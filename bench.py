@@ -335,7 +335,14 @@ def run_engine(args):
         outcome[v.name] = {"seeds": int(len(all_rows)), "t1_p99_ci_ms": cis[0], "t1_miss_ci": cis[1],
                            "miss_histogram_nonzero_bins": int((hist > 0).sum())}
     vi = {v.name: i for i, v in enumerate(vs)}
+    from paper_2508_20274_b200.api import hist_bin_edges
+
+    edges = hist_bin_edges()
     for name, i in vi.items():
+        # pooled t1 tail over all seeds (and ranks) from the reduced histogram, exact to the bin
+        ft = tids.index(focus)
+        outcome[name]["t1_pooled_p99_bin_ms"], outcome[name]["t1_pooled_p999_bin_ms"] = (
+            list(b) for b in sharding.pooled_quantiles(lat[i, ft], edges, (0.99, 0.999)))
         outcome[name]["window_completions"] = {tid: int(cnt[i, k, 1]) for k, tid in enumerate(tids)}
         outcome[name]["window_misses"] = {tid: int(cnt[i, k, 2]) for k, tid in enumerate(tids)}
     line = {

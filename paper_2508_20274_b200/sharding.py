@@ -107,3 +107,26 @@ def reduce_tenant_hists(lat_hist: np.ndarray, counts: np.ndarray, dist=None, dev
     dist.all_reduce(buf)
     out = buf.cpu().numpy()
     return out[: lat_hist.size].reshape(lat_hist.shape), out[lat_hist.size:].reshape(counts.shape)
+
+
+def pooled_quantiles(hist_row: np.ndarray, edges: np.ndarray, qs: Sequence[float] = (0.5, 0.95, 0.99, 0.999)
+                     ) -> List[Tuple[float, float]]:
+    """Pooled tail of one (variant, tenant) over every seed and rank: for each q, the latency bin
+    [lo, hi) that holds the nearest-rank q-quantile (rank = clamp(ceil(q * N), 1, N), the reference's
+    rule, telemetry.cpp:52-55) of ALL measurement-window latencies summed into `hist_row` (the
+    reduced lat_hist.h histogram, 64 bins per octave).  The SURVEY 8(f)3 p999 / TTFT extension for
+    C3 / C4: exact to the bin, from integer counts, so identical on any number of ranks.  `edges`:
+    api.hist_bin_edges() (bin lower edges); the first bin is open below, the last open above."""
+    h = np.asarray(hist_row, np.int64)
+    n = int(h.sum())
+    if n == 0:
+        return [(math.nan, math.nan) for _ in qs]
+    cum = np.cumsum(h)
+    out = []
+    for q in qs:
+        rank = min(max(int(math.ceil(q * n)), 1), n)
+        b = int(np.searchsorted(cum, rank))  # first bin whose cumulative count reaches the rank
+        lo = -math.inf if b == 0 else float(edges[b])
+        hi = math.inf if b + 1 >= len(edges) else float(edges[b + 1])
+        out.append((lo, hi))
+    return out

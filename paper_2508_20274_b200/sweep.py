@@ -140,6 +140,9 @@ def main(argv=None) -> None:
         dist.all_reduce(c)
         res["tenant_ticks"], res["completions"] = int(c[0]), int(c[1])
     if rank == 0:
+        from .api import hist_bin_edges
+
+        edges = hist_bin_edges()
         summary = {
             "scenario": args.scenario, "focus_tenant": res["focus_tenant"], "ranks": world, "seeds": args.seeds,
             "tenant_ticks": res["tenant_ticks"], "completions": res["completions"],
@@ -150,6 +153,11 @@ def main(argv=None) -> None:
                           "tenant_counts": {tid: [int(x) for x in v["tenant_counts"][i]]
                                             for i, tid in enumerate(res["tenant_ids"])},
                           "latency_hist_total": int(v["latency_hist"].sum()),
+                          # pooled p50/p95/p99/p999 over every seed's window latencies, exact to the bin
+                          "pooled_quantile_bins_ms": {
+                              tid: {name: list(b) for name, b in zip(("p50", "p95", "p99", "p999"),
+                                                                       sharding.pooled_quantiles(v["latency_hist"][i], edges))}
+                              for i, tid in enumerate(res["tenant_ids"])},
                           "miss_histogram_nonzero": {int(i): int(x) for i, x in enumerate(v["miss_histogram"]) if x}}
                          for v in res["variants"]],
         }

@@ -51,3 +51,23 @@ def test_latency_hist_matches_reference_completions(engine, path, variants):
         assert (cnt[v] == c).all(), f"variant {variants[v][0]}: counters differ {cnt[v]} vs {c}"
         # every window completion is in exactly one bin
         assert (lat[v].sum(1) == cnt[v][:, 1]).all()
+    # the pooled tail (SURVEY 8(f)3 p999 extension) brackets the exact pooled nearest rank of the
+    # reference's own window completions over all seeds
+    from paper_2508_20274_b200 import sharding
+    from paper_2508_20274_b200.api import hist_bin_edges
+
+    edges = hist_bin_edges()
+    for v, (_, ov) in enumerate(variants):
+        pooled = {ti: [] for ti in range(len(tids))}
+        for seed in seeds:
+            r, rc = ref_run(path, seed, ov, keep_completions=True)
+            win = rc["done"] >= r["summary"]["measure_start_s"]
+            for ti in range(len(tids)):
+                pooled[ti].append(rc["total"][win & (rc["tenant"] == ti)])
+        for ti in range(len(tids)):
+            vals = np.sort(np.concatenate(pooled[ti]))
+            if len(vals) == 0:
+                continue
+            for q, (lo, hi) in zip((0.5, 0.99, 0.999), sharding.pooled_quantiles(lat[v, ti], edges, (0.5, 0.99, 0.999))):
+                k = min(max(int(np.ceil(q * len(vals))), 1), len(vals))
+                assert lo <= vals[k - 1] < hi, (variants[v][0], tids[ti], q)

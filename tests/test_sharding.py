@@ -126,3 +126,23 @@ def test_two_rank_tenant_hists_equal_single_rank(n_seeds):
     for r in range(2):
         lat, cnt = out[r]
         assert lat.dtype == np.int64 and (lat == one[0]).all() and (cnt == one[1]).all()
+
+
+def test_pooled_quantiles_bracket_nearest_rank():
+    """sharding.pooled_quantiles: the bin it returns for q holds the exact pooled nearest-rank
+    q-quantile of the samples that were binned (telemetry.cpp:52-55 rule), incl. clamped end bins."""
+    from oracle import restate
+    from paper_2508_20274_b200.api import hist_bin_edges
+
+    edges = hist_bin_edges()
+    rng = np.random.default_rng(5)
+    for n in (1, 2, 7, 1000, 54321):
+        x = np.concatenate([rng.lognormal(1.5, 1.2, n), [1e-9, 5e7][: min(2, n // 500)]])
+        hist = np.bincount(restate.lat_bins(x), minlength=restate.HIST_BINS)
+        srt = np.sort(x)
+        qs = (0.5, 0.95, 0.99, 0.999)
+        for q, (lo, hi) in zip(qs, sharding.pooled_quantiles(hist, edges, qs)):
+            k = min(max(int(np.ceil(q * len(x))), 1), len(x))
+            v = srt[k - 1]
+            assert lo <= v < hi, (n, q, v, lo, hi)
+    assert all(np.isnan(a) for a in sharding.pooled_quantiles(np.zeros(restate.HIST_BINS, np.int64), edges)[0])

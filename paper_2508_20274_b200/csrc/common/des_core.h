@@ -292,9 +292,13 @@ MG_HD void hist_add(uint32_t* p, bool per_thread = false) {
 }
 
 // Execution model of a Lanes type: kPerThread = one thread runs one replica (no warp redundancy).
+// kDefer: the hot handlers queue the pipeline helpers as continuation ops (one copy each in the
+// event loop: the instruction-fetch-bound saturated regime) instead of inlining them per call site
+// (the latency-bound regime, where the op loop's extra instructions sit on the critical path).
 template <class Lanes>
 struct LanesTraits {
     static constexpr bool kPerThread = false;
+    static constexpr bool kDefer = true;
 };
 
 MG_HD void prefetch_l1(const void* p) {
@@ -734,7 +738,19 @@ struct Sim {
         Action a = on_observation(i, d.obs_lat, now, d.obs_arrived);
         if (a.valid) apply_action(a);
     }
-    // run the ops the handler queued, depth first (if-chain in frequency order: no indirect branch)
+    MG_HD void run_op(uint32_t code, int arg) {  // if-chain in frequency order: no indirect branch
+        if (code == kOpRealloc) reallocate_root(arg);
+        else if (code == kOpStartCompute) start_compute(arg);
+        else if (code == kOpStartTransfer) start_transfer_t<LanesTraits<Lanes>::kDefer>(arg);
+        else observe(arg);
+    }
+    // a helper call of a hot handler: queued (kDefer) or run in place (`code` is a literal at every
+    // call site, so the in-place form folds to the one helper)
+    MG_HD void call(uint32_t code, int arg) {
+        if (LanesTraits<Lanes>::kDefer) then(code, arg);
+        else run_op(code, arg);
+    }
+    // run the ops the handler queued, depth first
     MG_HD void run_ops() {
         ops = cont;
         cont = 0;
@@ -743,10 +759,7 @@ struct Sim {
             const uint32_t code = (ops >> 7) & 7u;
             const int arg = static_cast<int>(ops & 0x7fu);
             ops >>= 10;
-            if (code == kOpRealloc) reallocate_root(arg);
-            else if (code == kOpStartCompute) start_compute(arg);
-            else if (code == kOpStartTransfer) start_transfer_t<true>(arg);
-            else observe(arg);
+            run_op(code, arg);
             if (n_cont) {
                 if (n_cont > 3 || (ops >> (30 - 10 * n_cont)) != 0) st.error = kErrOpOverflow;
                 ops = cont | (ops << (10 * n_cont));
@@ -766,7 +779,7 @@ struct Sim {
         // start_transfer is deferred past the next-arrival push: only same-kind pushes compare by
         // seq, and their relative order is unchanged
         if (d.n_arrived < d.n_count) push(kEvArrival, i, io.arr_t[d.base + d.n_arrived]);
-        then(kOpStartTransfer, i);
+        call(kOpStartTransfer, i);
     }
 
     MG_HD void on_transfer_complete(int i) {
@@ -777,7 +790,7 @@ struct Sim {
         const bool done =
             rem <= kEpsBytes || (d.grant > 0.0 && fadd(now, fdiv_exact(rem, d.grant)) <= now);
         if (!done) {
-            then(kOpRealloc, r);
+            call(kOpRealloc, r);
             return;
         }
         d.remaining = 0.0;
@@ -786,9 +799,9 @@ struct Sim {
         io.req_transfer_ms[d.base + k] = fadd(d.transfer_ms, fmul(fsub(now, d.started_s), 1000.0));
         rd[r].active &= ~(1ull << i);
         d.grant = 0.0;
-        then(kOpRealloc, r);
-        then(kOpStartCompute, i);
-        then(kOpStartTransfer, i);
+        call(kOpRealloc, r);
+        call(kOpStartCompute, i);
+        call(kOpStartTransfer, i);
     }
 
     MG_HD void on_compute_complete(int i) {
@@ -826,11 +839,11 @@ struct Sim {
         }
         st.done_seq += 1;
         if (io.tr_win) tw_push(io.tr_win[i], total);
-        then(kOpStartCompute, i);
+        call(kOpStartCompute, i);
         if (C.enabled) {
             d.obs_lat = total;
             d.obs_arrived = arrived;
-            then(kOpObserve, i);
+            call(kOpObserve, i);
         }
     }
 
@@ -1634,7 +1647,7 @@ struct Sim {
             case kEvArrival: on_arrival(i); break;
             default: on_tick(); break;
         }
-        run_ops();
+        if (LanesTraits<Lanes>::kDefer) run_ops();
     }
 
     // host event loop (engine.cpp:864-894); the device loop lives in des_kernel

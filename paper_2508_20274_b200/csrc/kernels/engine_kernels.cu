@@ -97,6 +97,17 @@ template <>
 struct MaskOf<RegLanes> {
     using type = uint32_t;  // T <= kRegSlotMaxTenants
 };
+// the same lanes with the pipeline helpers inlined at their call sites (latency-bound batches)
+struct RegLanesDirect : RegLanes {};
+template <>
+struct MaskOf<RegLanesDirect> {
+    using type = uint32_t;
+};
+template <>
+struct LanesTraits<RegLanesDirect> {
+    static constexpr bool kPerThread = false;
+    static constexpr bool kDefer = false;
+};
 
 template <class Lanes>
 __device__ __forceinline__ Lanes make_lanes(unsigned char* smem, const SimLayout& L, int T);
@@ -112,15 +123,32 @@ __device__ __forceinline__ RegLanes make_lanes<RegLanes>(unsigned char*, const S
     r.hh = r.hl = r.hq = r.rh = r.rl = r.rq = 0xffffffffu;
     return r;
 }
+template <>
+__device__ __forceinline__ RegLanesDirect make_lanes<RegLanesDirect>(unsigned char* smem, const SimLayout& L, int T) {
+    RegLanesDirect r;
+    static_cast<RegLanes&>(r) = make_lanes<RegLanes>(smem, L, T);
+    return r;
+}
 
 // Warp argmin of the next event.  Returns false when no live event is left.  On success every
 // lane holds the winner's slot index and (t, q).
 template <class Lanes>
 __device__ __forceinline__ bool next_event(Sim<Lanes>& sim, int T, int& s_out, double& t_out, uint32_t& q_out);
 
+template <class SimT>
+__device__ __forceinline__ bool reg_next_event(SimT& sim, int& s_out, double& t_out, uint32_t& q_out);
 template <>
 __device__ __forceinline__ bool next_event<RegLanes>(Sim<RegLanes>& sim, int, int& s_out, double& t_out,
                                                      uint32_t& q_out) {
+    return reg_next_event(sim, s_out, t_out, q_out);
+}
+template <>
+__device__ __forceinline__ bool next_event<RegLanesDirect>(Sim<RegLanesDirect>& sim, int, int& s_out, double& t_out,
+                                                           uint32_t& q_out) {
+    return reg_next_event(sim, s_out, t_out, q_out);
+}
+template <class SimT>
+__device__ __forceinline__ bool reg_next_event(SimT& sim, int& s_out, double& t_out, uint32_t& q_out) {
     RegLanes& R = sim.lanes;
     uint32_t h = R.hh, l = R.hl, q = R.hq;
     int s = R.lane;
@@ -353,15 +381,16 @@ __global__ void MG_DESK_BOUNDS des_kernel(const PScenario* __restrict__ S, const
     des_body<HostLanes, true>(S, C, B, n_rep, L);
 }
 
-#ifdef MG_DES_MAXNREG
-#define MG_DES_BOUNDS __maxnreg__(MG_DES_MAXNREG)
-#else
-#define MG_DES_BOUNDS __launch_bounds__(32)
+// the latency-regime kernel: helpers inlined at their call sites (RegLanesDirect) and a register
+// budget large enough that ptxas does not spill (it settles on 128 + spills under launch_bounds)
+#ifndef MG_DES_MAXNREG
+#define MG_DES_MAXNREG 168
 #endif
+#define MG_DES_BOUNDS __maxnreg__(MG_DES_MAXNREG)
 __global__ void MG_DES_BOUNDS des_kernel_reg(const PScenario* __restrict__ S,
                                                      const PController* __restrict__ C, WaveBuffers B, int n_rep,
                                                      SimLayout L) {
-    des_body<RegLanes>(S, C, B, n_rep, L);
+    des_body<RegLanesDirect>(S, C, B, n_rep, L);
 }
 // Saturated regime: with the event loop no longer instruction-fetch bound (continuation ops),
 // dependent-latency stalls dominate and twice the resident warps hide them (C4 wave: 780 -> 676 ms
@@ -405,6 +434,7 @@ struct MaskOf<SimtLanes> {
 template <>
 struct LanesTraits<SimtLanes> {
     static constexpr bool kPerThread = true;
+    static constexpr bool kDefer = true;
 };
 
 __global__ void __launch_bounds__(kSimtBlock) des_simt_kernel(const PScenario* __restrict__ S,

@@ -9,6 +9,6 @@ for arm in "${A[@]}"; do
   if [ -n "$lv" ]; then L=$PWD/build/var$lv/libmigsim_b200.so; else L=""; fi
   for a in ${SHAPES:-"scenarios/exp/default_300s.yaml:4736" "tests/golden/scenarios/default.yaml:2368"}; do
     sc=${a%%:*}; n=${a##*:}
-    env $envs MIGSIM_LIB=$L timeout 600 python tools/ab_des.py $sc $n c4 warp 2 2>&1 | tail -1 | sed "s/^/$name /"
+    env $envs MIGSIM_LIB=$L timeout 600 python tools/ab_des.py $sc $n ${VSET:-c4} warp 2 2>&1 | tail -1 | sed "s/^/$name /"
   done
 done | tee gpurun_out/ab_env.txt

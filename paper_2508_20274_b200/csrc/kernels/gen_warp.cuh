@@ -27,7 +27,7 @@ constexpr int kRing = 512;
 static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
 // ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
 __device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
-constexpr int kMaxCallsRound = 80;  // gamma calls scanned per round (keeps the block at 15.6 KB: 14 warps/SM)
+constexpr int kMaxCallsRound = 80;  // gamma calls scanned per round (keeps the block at 11.5 KB: 18 warps/SM)
 
 struct WarpMtSmem {
     uint64_t x[kMtN];
@@ -159,8 +159,9 @@ __device__ void warp_gen_marks(WarpMtSmem& m, int purpose, const PTenant& p, uin
 struct GammaSmem {
     WarpMtSmem mt;
     double c[kRing];    // canonical at position p (ring)
-    double ny[kRing];   // y*mult if the pair starting at p is accepted, NaN if it is rejected
-    double nx[kRing];   // x*mult (the polar cache)
+    double pm[kRing];   // polar multiplier of the pair starting at p if it is accepted, NaN if rejected;
+                        // the scan forms y*mult / x*mult from c[] with the same two roundings, so the
+                        // ring holds one word per position instead of two (18 instead of 14 warps/SM)
     double call_v[kMaxCallsRound];  // the call's v, then (in place) its gap value
     int16_t call_q[kMaxCallsRound];  // ring index of the call's pow uniform, -1: none
     int32_t n_calls;
@@ -179,13 +180,8 @@ __device__ __forceinline__ void gamma_fill(GammaSmem& g, int64_t gen_end, int la
         const double y = fsub(fmul(2.0, g.c[ring_idx(pos + 1)]), 1.0);
         const double r2 = fadd(fmul(x, x), fmul(y, y));
         const bool a = !(r2 > 1.0 || r2 == 0.0);
-        if (a) {
-            const double mult = fsqrt(fdiv_exact(fmul(-2.0, gl_log(r2)), r2));
-            g.ny[ring_idx(pos)] = fmul(y, mult);
-            g.nx[ring_idx(pos)] = fmul(x, mult);
-        } else {
-            g.ny[ring_idx(pos)] = k_nan();  // an accepted pair's normals are finite
-        }
+        // an accepted pair's multiplier is finite
+        g.pm[ring_idx(pos)] = a ? fsqrt(fdiv_exact(fmul(-2.0, gl_log(r2)), r2)) : k_nan();
     }
     __syncwarp();
 }
@@ -196,20 +192,24 @@ __device__ __forceinline__ bool gamma_scan_call(const GammaSmem& g, const GammaP
                                                 double& v_out, int32_t& q_out) {
     int64_t p = pos;
     bool cached = false;
-    double cache = 0.0, n, v, u;
+    double cache_m = 0.0, n, v, u;
+    uint32_t cache_i = 0;
     for (;;) {
         do {
             if (cached) {
-                n = cache;
+                n = fmul(fsub(fmul(2.0, g.c[cache_i]), 1.0), cache_m);  // x * mult
                 cached = false;
             } else {
+                double m;
                 for (;;) {
                     if (p + 1 >= limit) return false;
-                    n = g.ny[ring_idx(p)];
-                    if (n == n) break;  // accepted pair
+                    m = g.pm[ring_idx(p)];
+                    if (m == m) break;  // accepted pair
                     p += 2;
                 }
-                cache = g.nx[ring_idx(p)];
+                n = fmul(fsub(fmul(2.0, g.c[ring_idx(p + 1)]), 1.0), m);  // y * mult
+                cache_m = m;
+                cache_i = ring_idx(p);
                 cached = true;
                 p += 2;
             }

@@ -162,9 +162,11 @@ struct GammaSmem {
     double pm[kRing];   // polar multiplier of the pair starting at p if it is accepted, NaN if rejected;
                         // the scan forms y*mult / x*mult from c[] with the same two roundings, so the
                         // ring holds one word per position instead of two (18 instead of 14 warps/SM)
-    double call_v[kMaxCallsRound];  // the call's v, then (in place) its gap value
-    int16_t call_q[kMaxCallsRound];  // ring index of the call's pow uniform, -1: none
+    double call_v[kMaxCallsRound];  // the call's gap value, then (in place) its clock
+    int16_t call_q[kMaxCallsRound];  // ring index of the call's first position
+    uint8_t nxt[kRing];  // positions consumed by a call starting here: 0 = not known yet, 255 = long
     int32_t n_calls;
+    int32_t n_valid;  // calls whose clock is inside the horizon and the capacity (this round)
 };
 
 // Generate the next 312 canonicals at positions [gen_end, gen_end+312) and the speculative pair
@@ -276,6 +278,7 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
     warp_mt_seed(g.mt, seed_word, lane);
     int64_t gen_end = 0;  // canonicals known for positions < gen_end
     int64_t pos = 0;      // stream position of the next call
+    int64_t evald = 0;    // call lengths (nxt) are known for the positions in [pos, evald)
     gamma_fill(g, gen_end, lane);
     gen_end += kMtN;
     bool done = false;
@@ -285,17 +288,44 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
             gamma_fill(g, gen_end, lane);
             gen_end += kMtN;
         }
-        // lane 0: scan calls (cheap arithmetic) while the ring holds their positions
-        if (lane == 0) {
-            int32_t nc = 0;
-            const int64_t limit = gen_end - 1;  // pair transforms exist below gen_end-1
-            while (nc < kMaxCallsRound && pos + 1 < limit && limit - pos > 64) {
-                int64_t pp = pos;
+        const int64_t limit = gen_end - 1;  // pair transforms exist below gen_end-1
+        // speculative scan, lane-parallel: the rejection loop of a call starting at EVERY position
+        // not evaluated yet (only the consumption length is kept); evaluations that would read past
+        // `limit` stay unknown and are redone after the next fill
+        {
+            const int64_t from = evald > pos ? evald : pos;
+            int64_t first_unknown = limit;
+            for (int64_t p0 = from + lane; p0 < limit; p0 += 32) {
+                int64_t pp = p0;
                 double v;
                 int32_t q;
-                if (!gamma_scan_call(g, gp, pp, limit, v, q)) break;
-                g.call_v[nc] = v;
-                g.call_q[nc] = static_cast<int16_t>(q);
+                uint8_t d = 0;
+                if (gamma_scan_call(g, gp, pp, limit, v, q)) d = pp - p0 < 255 ? static_cast<uint8_t>(pp - p0) : 255;
+                else first_unknown = p0 < first_unknown ? p0 : first_unknown;
+                g.nxt[ring_idx(p0)] = d;
+            }
+            // every position below evald has a known length
+            const int64_t fu = first_unknown;
+            uint32_t hi = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(static_cast<uint64_t>(fu) >> 32));
+            uint32_t lo = __reduce_min_sync(0xffffffffu, static_cast<uint32_t>(static_cast<uint64_t>(fu) >> 32) == hi
+                                                            ? static_cast<uint32_t>(fu) : 0xffffffffu);
+            evald = static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
+        }
+        __syncwarp();
+        // lane 0: walk the calls through the lengths (one shared-memory load per call)
+        if (lane == 0) {
+            int32_t nc = 0;
+            while (nc < kMaxCallsRound && pos + 1 < limit && limit - pos > 64 && pos < evald) {
+                const uint8_t d = g.nxt[ring_idx(pos)];
+                int64_t pp = pos;
+                if (d == 255) {  // a call longer than 254 positions (never seen): scanned in place
+                    double v;
+                    int32_t q;
+                    if (!gamma_scan_call(g, gp, pp, limit, v, q)) break;
+                } else {
+                    pp += d;
+                }
+                g.call_q[nc] = static_cast<int16_t>(ring_idx(pos));
                 ++nc;
                 pos = pp;
             }
@@ -304,38 +334,59 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         __syncwarp();
         pos = __shfl_sync(0xffffffffu, pos, 0);
         const int32_t nc = g.n_calls;
-        // lane-parallel gap values: pow(u, 1/alpha) * a1 * v * beta (random.tcc:2382-2392)
+        // lane-parallel: each walked call's v and pow uniform again (the same loop on the same ring
+        // words), then its gap value pow(u, 1/alpha) * a1 * v * beta (random.tcc:2382-2392)
         for (int k = lane; k < nc; k += 32) {
-            const double v = g.call_v[k];
-            if (g.call_q[k] < 0) g.call_v[k] = fmul(fmul(gp.a1, v), gp.beta);
-            else g.call_v[k] = fmul(fmul(fmul(gl_pow(g.c[g.call_q[k]], gp.inv_alpha), gp.a1), v), gp.beta);
+            int64_t pp = g.call_q[k];  // ring index as the position: ring_idx masks the same way
+            double v;
+            int32_t q;
+            gamma_scan_call(g, gp, pp, pp + kRing, v, q);
+            if (q < 0) g.call_v[k] = fmul(fmul(gp.a1, v), gp.beta);
+            else g.call_v[k] = fmul(fmul(fmul(gl_pow(g.c[q], gp.inv_alpha), gp.a1), v), gp.beta);
         }
         __syncwarp();
-        // lane 0: the clock is an ordered FP sum (workload.cpp:135)
+        // lane 0: the clock is an ordered FP sum (workload.cpp:135), written over the gap values
         if (lane == 0) {
-            for (int32_t k = 0; k < nc; ++k) {
-                clock = fadd(clock, g.call_v[k]);
-                if (clock >= duration) {
+            int32_t nv = 0;
+            for (; nv < nc; ++nv) {
+                const double c = fadd(clock, g.call_v[nv]);
+                if (c >= duration) {
                     done = true;
                     break;
                 }
-                if (na >= cap) {
+                if (na + nv >= cap) {
                     ok = false;
                     done = true;
                     break;
                 }
-                // the unthinned clock is read back only for thinned tenants (gen_marks)
-                if (thinned) {
-                    t_all[na] = clock;
-                    if (sched_active(p.sched, clock)) t_kept[nk++] = clock;
-                } else {
-                    t_kept[nk++] = clock;
-                }
-                ++na;
+                clock = c;
+                g.call_v[nv] = c;
             }
+            g.n_valid = nv;
         }
+        __syncwarp();
         done = __shfl_sync(0xffffffffu, done, 0);
         ok = __shfl_sync(0xffffffffu, ok, 0);
+        // the round's arrival times, stored lane-parallel (the unthinned clock is read back only
+        // for thinned tenants, by gen_marks)
+        const int32_t nv = g.n_valid;
+        if (thinned) {
+            for (int32_t k0 = 0; k0 < nv; k0 += 32) {
+                const int32_t k = k0 + lane;
+                const bool valid = k < nv;
+                const double c = valid ? g.call_v[k] : 0.0;
+                if (valid) t_all[na + k] = c;
+                const bool keep = valid && sched_active(p.sched, c);
+                const unsigned mk = __ballot_sync(0xffffffffu, keep);
+                if (keep) t_kept[nk + __popc(mk & lanemask_lt(lane))] = c;
+                nk += __popc(mk);
+            }
+        } else {
+            for (int32_t k = lane; k < nv; k += 32) t_kept[nk + k] = g.call_v[k];
+            nk += nv;
+        }
+        na += nv;
+        __syncwarp();
         if (!done && nc == 0) {
             // one call needs more than the lookahead (~10^-200 probability): widen the window
             // while the ring can hold it, otherwise report instead of reading stale positions

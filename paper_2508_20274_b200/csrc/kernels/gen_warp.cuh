@@ -164,7 +164,8 @@ struct GammaSmem {
                         // ring holds one word per position instead of two (18 instead of 14 warps/SM)
     double call_v[kMaxCallsRound];  // the call's gap value, then (in place) its clock
     int16_t call_q[kMaxCallsRound];  // ring index of the call's first position
-    uint8_t nxt[kRing];  // positions consumed by a call starting here: 0 = not known yet, 255 = long
+    uint8_t nxt[kRing];   // positions consumed by a call starting here: 0 = not known yet, 255 = long
+    uint8_t nxt2[kRing];  // ... by the two calls starting here (0 = not known / too long)
     int32_t n_calls;
     int32_t n_valid;  // calls whose clock is inside the horizon and the capacity (this round)
 };
@@ -292,6 +293,7 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         // speculative scan, lane-parallel: the rejection loop of a call starting at EVERY position
         // not evaluated yet (only the consumption length is kept); evaluations that would read past
         // `limit` stay unknown and are redone after the next fill
+        const int64_t ev0 = evald;
         {
             const int64_t from = evald > pos ? evald : pos;
             int64_t first_unknown = limit;
@@ -312,11 +314,37 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
             evald = static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
         }
         __syncwarp();
-        // lane 0: walk the calls through the lengths (one shared-memory load per call)
+        // two-call lengths where both are known (positions below ev0 - 32 kept theirs from earlier
+        // rounds; a length still unknown there only costs the walk a single step)
+        {
+            const int64_t f2 = ev0 - 32 > pos ? ev0 - 32 : pos;
+            for (int64_t p0 = f2 + lane; p0 < evald; p0 += 32) {
+                const uint32_t d1 = g.nxt[ring_idx(p0)];
+                uint32_t d2 = 0;
+                if (d1 != 255 && p0 + d1 < evald) {
+                    const uint32_t e = g.nxt[ring_idx(p0 + d1)];
+                    if (e != 255 && d1 + e < 255) d2 = d1 + e;
+                }
+                g.nxt2[ring_idx(p0)] = static_cast<uint8_t>(d2);
+            }
+        }
+        __syncwarp();
+        // lane 0: walk the calls through the lengths (one shared-memory load per one or two calls;
+        // the start of a jumped-over call is filled in lane-parallel below, marked -1)
         if (lane == 0) {
             int32_t nc = 0;
-            while (nc < kMaxCallsRound && pos + 1 < limit && limit - pos > 64 && pos < evald) {
-                const uint8_t d = g.nxt[ring_idx(pos)];
+            const int64_t stop = evald < limit - 64 ? evald : limit - 64;
+            while (nc < kMaxCallsRound && pos < stop) {
+                const uint32_t ri = ring_idx(pos);
+                const uint32_t d2 = g.nxt2[ri];
+                g.call_q[nc] = static_cast<int16_t>(ri);
+                if (d2 != 0 && nc + 1 < kMaxCallsRound) {
+                    g.call_q[nc + 1] = -1;
+                    nc += 2;
+                    pos += d2;
+                    continue;
+                }
+                const uint32_t d = g.nxt[ri];
                 int64_t pp = pos;
                 if (d == 255) {  // a call longer than 254 positions (never seen): scanned in place
                     double v;
@@ -325,7 +353,6 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                 } else {
                     pp += d;
                 }
-                g.call_q[nc] = static_cast<int16_t>(ring_idx(pos));
                 ++nc;
                 pos = pp;
             }
@@ -337,7 +364,12 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         // lane-parallel: each walked call's v and pow uniform again (the same loop on the same ring
         // words), then its gap value pow(u, 1/alpha) * a1 * v * beta (random.tcc:2382-2392)
         for (int k = lane; k < nc; k += 32) {
-            int64_t pp = g.call_q[k];  // ring index as the position: ring_idx masks the same way
+            int32_t st = g.call_q[k];
+            if (st < 0) {
+                const int32_t pr = g.call_q[k - 1];
+                st = static_cast<int32_t>(ring_idx(pr + g.nxt[pr]));
+            }
+            int64_t pp = st;  // ring index as the position: ring_idx masks the same way
             double v;
             int32_t q;
             gamma_scan_call(g, gp, pp, pp + kRing, v, q);
@@ -347,20 +379,21 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         __syncwarp();
         // lane 0: the clock is an ordered FP sum (workload.cpp:135), written over the gap values
         if (lane == 0) {
+            const int32_t lim = cap - na < nc ? static_cast<int32_t>(cap - na) : nc;  // capacity left
             int32_t nv = 0;
-            for (; nv < nc; ++nv) {
+            for (; nv < lim; ++nv) {
                 const double c = fadd(clock, g.call_v[nv]);
                 if (c >= duration) {
                     done = true;
                     break;
                 }
-                if (na + nv >= cap) {
-                    ok = false;
-                    done = true;
-                    break;
-                }
                 clock = c;
                 g.call_v[nv] = c;
+            }
+            // the call at the capacity: past the horizon ends the stream, else it overflows
+            if (!done && nv < nc) {
+                if (!(fadd(clock, g.call_v[nv]) >= duration)) ok = false;
+                done = true;
             }
             g.n_valid = nv;
         }

@@ -165,7 +165,7 @@ struct GammaSmem {
     double call_v[kMaxCallsRound];  // the call's gap value, then (in place) its clock
     int16_t call_q[kMaxCallsRound];  // ring index of the call's first position
     uint8_t nxt[kRing];   // positions consumed by a call starting here: 0 = not known yet, 255 = long
-    uint8_t nxt2[kRing];  // ... by the two calls starting here (0 = not known / too long)
+    uint8_t nxt4[kRing];  // ... by the four calls starting here (0 = not known / too long)
     int32_t n_calls;
     int32_t n_valid;  // calls whose clock is inside the horizon and the capacity (this round)
 };
@@ -314,34 +314,38 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
             evald = static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
         }
         __syncwarp();
-        // two-call lengths where both are known (positions below ev0 - 32 kept theirs from earlier
-        // rounds; a length still unknown there only costs the walk a single step)
+        // four-call lengths where all four are known (positions below ev0 - 64 kept theirs from
+        // earlier rounds; a length still unknown there only costs the walk single steps)
         {
-            const int64_t f2 = ev0 - 32 > pos ? ev0 - 32 : pos;
-            for (int64_t p0 = f2 + lane; p0 < evald; p0 += 32) {
-                const uint32_t d1 = g.nxt[ring_idx(p0)];
-                uint32_t d2 = 0;
-                if (d1 != 255 && p0 + d1 < evald) {
-                    const uint32_t e = g.nxt[ring_idx(p0 + d1)];
-                    if (e != 255 && d1 + e < 255) d2 = d1 + e;
+            const int64_t f4 = ev0 - 64 > pos ? ev0 - 64 : pos;
+            for (int64_t p0 = f4 + lane; p0 < evald; p0 += 32) {
+                uint32_t dsum = 0;
+                int j = 0;
+                for (; j < 4; ++j) {
+                    if (p0 + dsum >= evald) break;
+                    const uint32_t d = g.nxt[ring_idx(p0 + dsum)];
+                    if (d == 255) break;
+                    dsum += d;
                 }
-                g.nxt2[ring_idx(p0)] = static_cast<uint8_t>(d2);
+                g.nxt4[ring_idx(p0)] = static_cast<uint8_t>(j == 4 && dsum < 255 ? dsum : 0);
             }
         }
         __syncwarp();
-        // lane 0: walk the calls through the lengths (one shared-memory load per one or two calls;
-        // the start of a jumped-over call is filled in lane-parallel below, marked -1)
+        // lane 0: walk the calls through the lengths (one shared-memory load per one or four calls;
+        // the starts of jumped-over calls are filled in lane-parallel below, marked -1..-3)
         if (lane == 0) {
             int32_t nc = 0;
             const int64_t stop = evald < limit - 64 ? evald : limit - 64;
             while (nc < kMaxCallsRound && pos < stop) {
                 const uint32_t ri = ring_idx(pos);
-                const uint32_t d2 = g.nxt2[ri];
+                const uint32_t d4 = g.nxt4[ri];
                 g.call_q[nc] = static_cast<int16_t>(ri);
-                if (d2 != 0 && nc + 1 < kMaxCallsRound) {
+                if (d4 != 0 && nc + 3 < kMaxCallsRound) {
                     g.call_q[nc + 1] = -1;
-                    nc += 2;
-                    pos += d2;
+                    g.call_q[nc + 2] = -2;
+                    g.call_q[nc + 3] = -3;
+                    nc += 4;
+                    pos += d4;
                     continue;
                 }
                 const uint32_t d = g.nxt[ri];
@@ -366,8 +370,9 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         for (int k = lane; k < nc; k += 32) {
             int32_t st = g.call_q[k];
             if (st < 0) {
-                const int32_t pr = g.call_q[k - 1];
-                st = static_cast<int32_t>(ring_idx(pr + g.nxt[pr]));
+                const int j = -st;
+                st = g.call_q[k - j];
+                for (int i = 0; i < j; ++i) st = static_cast<int32_t>(ring_idx(st + g.nxt[st]));
             }
             int64_t pp = st;  // ring index as the position: ring_idx masks the same way
             double v;
@@ -378,28 +383,35 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
         }
         __syncwarp();
         // lane 0: the clock is an ordered FP sum (workload.cpp:135), written over the gap values
+        // (only the dependent adds; the horizon and capacity are found lane-parallel after)
         if (lane == 0) {
-            const int32_t lim = cap - na < nc ? static_cast<int32_t>(cap - na) : nc;  // capacity left
-            int32_t nv = 0;
-            for (; nv < lim; ++nv) {
-                const double c = fadd(clock, g.call_v[nv]);
-                if (c >= duration) {
-                    done = true;
-                    break;
-                }
-                clock = c;
-                g.call_v[nv] = c;
+#pragma unroll 4
+            for (int32_t k = 0; k < nc; ++k) {
+                clock = fadd(clock, g.call_v[k]);
+                g.call_v[k] = clock;
             }
-            // the call at the capacity: past the horizon ends the stream, else it overflows
-            if (!done && nv < nc) {
-                if (!(fadd(clock, g.call_v[nv]) >= duration)) ok = false;
-                done = true;
-            }
-            g.n_valid = nv;
         }
         __syncwarp();
-        done = __shfl_sync(0xffffffffu, done, 0);
-        ok = __shfl_sync(0xffffffffu, ok, 0);
+        {
+            int32_t kd = nc;  // first call at or past the horizon
+            for (int32_t k0 = 0; k0 < nc; k0 += 32) {
+                const unsigned m = __ballot_sync(0xffffffffu, k0 + lane < nc && g.call_v[k0 + lane] >= duration);
+                if (m) {
+                    kd = k0 + __ffs(m) - 1;
+                    break;
+                }
+            }
+            const int32_t lim = cap - na < nc ? static_cast<int32_t>(cap - na) : nc;  // capacity left
+            if (kd <= lim) {
+                if (kd < nc) done = true;
+                if (lane == 0) g.n_valid = kd;
+            } else {  // the capacity is reached before the horizon
+                ok = false;
+                done = true;
+                if (lane == 0) g.n_valid = lim;
+            }
+        }
+        __syncwarp();
         // the round's arrival times, stored lane-parallel (the unthinned clock is read back only
         // for thinned tenants, by gen_marks)
         const int32_t nv = g.n_valid;

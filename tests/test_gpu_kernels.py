@@ -52,8 +52,9 @@ def test_device_fmod_fast_exact(engine):
     assert same.all(), (x[~same][:5], y[~same][:5], out[~same][:5], ref[~same][:5])
 
 
-@pytest.mark.parametrize("path", GOLDEN_SCENARIOS + CONFIG_SCENARIOS)
-def test_device_arrivals_bit_exact(engine, path):
+def _arrivals_match(engine, path, seeds):
+    """Every tenant's device arrival records (time, bytes, service multiplier, noise) equal the
+    reference's ArrivalGen stream (workload.cpp:103-157) bit for bit."""
     lib = engine._lib
     lib.migsim_gpu_arrivals.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_uint64, ctypes.c_int32,
                                         ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
@@ -61,7 +62,8 @@ def test_device_arrivals_bit_exact(engine, path):
     sid = engine.load_scenario(path)
     ids = engine.tenant_ids(sid)
     spec = json.loads(ctypes.string_at(oracle().ref_scenario_dump(scenario_json(path), b"x")).decode())
-    for seed in (1, 23):
+    total = 0
+    for seed in seeds:
         for ti, tid in enumerate(ids):
             cap = 2_000_000
             ref = np.zeros((cap, 4))
@@ -72,8 +74,30 @@ def test_device_arrivals_bit_exact(engine, path):
             err = ctypes.create_string_buffer(512)
             assert lib.migsim_gpu_arrivals(engine._h, sid, seed, ti, mine.ctypes.data, cap, ctypes.byref(m), err,
                                            512) == 0, err.value
-            assert m.value == n
-            assert (ref[:n].view(np.uint64) == mine[:n].view(np.uint64)).all(), (tid, seed)
+            assert m.value == n, (path, tid, seed)
+            assert (ref[:n].view(np.uint64) == mine[:n].view(np.uint64)).all(), (path, tid, seed)
+            total += n
+    return total
+
+
+def test_device_arrivals_fuzz(engine, tmp_path):
+    """The generator's speculative scan / call walk / ordered clock over the fuzz corpus: gamma shapes
+    below and above 1 (arrival_cv 0.5-1.5: the pow boost on and off), deterministic clocks, phase and
+    square-wave thinning, size mixes, service and noise marks; 3 seeds per scenario."""
+    from tests.fuzz_scenarios import make_scenario
+
+    total = 0
+    for k in range(80):
+        path = str(tmp_path / f"a{k}.yaml")
+        with open(path, "w") as f:
+            f.write(make_scenario(7000 + k, wide=k % 4 == 3))
+        total += _arrivals_match(engine, path, (1 + k % 7, 40 + k, 1000 + 3 * k))
+    assert total > 0
+
+
+@pytest.mark.parametrize("path", GOLDEN_SCENARIOS + CONFIG_SCENARIOS)
+def test_device_arrivals_bit_exact(engine, path):
+    _arrivals_match(engine, path, (1, 23))
 
 
 def test_select_matches_nearest_rank(engine):

@@ -11,10 +11,12 @@
 //  * service (lognormal): each call starts with a fresh polar cache and consumes whole pairs, so
 //    pairs are aligned on even stream positions; accepted pairs are ranked with ballots.
 //  * arrival clock (gamma, Marsaglia-Tsang + pow boost): consumption is irregular, so the warp
-//    speculatively evaluates the polar transform for EVERY stream position (acc/ny/nx), lane 0
-//    walks the calls with cheap arithmetic only (the rare squeeze-rejection logs on demand), and
-//    the pow(u, 1/alpha) of every call is evaluated lane-parallel afterwards; lane 0 finally
-//    accumulates the clock in order (the FP sum order of workload.cpp:135).
+//    speculatively evaluates the polar multiplier of the pair at EVERY stream position, then the
+//    whole rejection loop of a call starting at every position (lane-parallel; only the number of
+//    positions it consumes is kept, plus the length of 4 consecutive calls); lane 0 walks the
+//    actual calls through those lengths (one shared-memory load per 4 calls), the walked calls'
+//    v and pow(u, 1/alpha) are evaluated lane-parallel, lane 0 accumulates the clock in order
+//    (the FP sum order of workload.cpp:135) and the lanes store the arrival times.
 #pragma once
 
 #include "../common/arrivals.h"
@@ -22,12 +24,12 @@
 namespace mg {
 
 // canonical ring (positions): one 312-word block is written per fill, so the scan may look ahead
-// kRing - kMtN positions; 512 keeps the block's shared memory at ~17 KB (12 resident warps/SM)
+// kRing - kMtN positions; 512 keeps the block's shared memory at 12.5 KB (17 resident warps/SM)
 constexpr int kRing = 512;
 static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
 // ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
 __device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
-constexpr int kMaxCallsRound = 80;  // gamma calls scanned per round (keeps the block at 11.5 KB: 18 warps/SM)
+constexpr int kMaxCallsRound = 80;  // gamma calls walked per round (~one 312-position fill)
 
 struct WarpMtSmem {
     uint64_t x[kMtN];
@@ -161,7 +163,7 @@ struct GammaSmem {
     double c[kRing];    // canonical at position p (ring)
     double pm[kRing];   // polar multiplier of the pair starting at p if it is accepted, NaN if rejected;
                         // the scan forms y*mult / x*mult from c[] with the same two roundings, so the
-                        // ring holds one word per position instead of two (18 instead of 14 warps/SM)
+                        // ring holds one word per position instead of two
     double call_v[kMaxCallsRound];  // the call's gap value, then (in place) its clock
     int16_t call_q[kMaxCallsRound];  // ring index of the call's first position
     uint8_t nxt[kRing];   // positions consumed by a call starting here: 0 = not known yet, 255 = long

@@ -29,6 +29,13 @@ constexpr int kRing = 512;
 static_assert((kRing & (kRing - 1)) == 0, "ring index by mask");
 // ring slot of a stream position (positions are >= 0: a mask, not a signed modulo)
 __device__ __forceinline__ uint32_t ring_idx(int64_t p) { return static_cast<uint32_t>(p) & (kRing - 1u); }
+// a call consuming kLongCall or more positions is marked long and scanned in place by lane 0 (never
+// seen at 255; test builds lower it with -DMG_GEN_LONG_CALL to exercise that path)
+#ifndef MG_GEN_LONG_CALL
+#define MG_GEN_LONG_CALL 255
+#endif
+constexpr uint32_t kLongCall = MG_GEN_LONG_CALL;
+static_assert(kLongCall >= 4 && kLongCall <= 255, "call lengths are stored in one byte");
 constexpr int kMaxCallsRound = 80;  // gamma calls walked per round (~one 312-position fill)
 
 struct WarpMtSmem {
@@ -166,7 +173,7 @@ struct GammaSmem {
                         // ring holds one word per position instead of two
     double call_v[kMaxCallsRound];  // the call's gap value, then (in place) its clock
     int16_t call_q[kMaxCallsRound];  // ring index of the call's first position
-    uint8_t nxt[kRing];   // positions consumed by a call starting here: 0 = not known yet, 255 = long
+    uint8_t nxt[kRing];   // positions consumed by a call starting here: 0 = not known yet, kLongCall = long
     uint8_t nxt4[kRing];  // ... by the four calls starting here (0 = not known / too long)
     int32_t n_calls;
     int32_t n_valid;  // calls whose clock is inside the horizon and the capacity (this round)
@@ -304,7 +311,7 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                 double v;
                 int32_t q;
                 uint8_t d = 0;
-                if (gamma_scan_call(g, gp, pp, limit, v, q)) d = pp - p0 < 255 ? static_cast<uint8_t>(pp - p0) : 255;
+                if (gamma_scan_call(g, gp, pp, limit, v, q)) d = static_cast<uint8_t>(pp - p0 < kLongCall ? pp - p0 : kLongCall);
                 else first_unknown = p0 < first_unknown ? p0 : first_unknown;
                 g.nxt[ring_idx(p0)] = d;
             }
@@ -326,7 +333,7 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                 for (; j < 4; ++j) {
                     if (p0 + dsum >= evald) break;
                     const uint32_t d = g.nxt[ring_idx(p0 + dsum)];
-                    if (d == 255) break;
+                    if (d == kLongCall) break;
                     dsum += d;
                 }
                 g.nxt4[ring_idx(p0)] = static_cast<uint8_t>(j == 4 && dsum < 255 ? dsum : 0);
@@ -352,7 +359,7 @@ __device__ bool warp_gen_times(GammaSmem& g, const PTenant& p, uint64_t seed_wor
                 }
                 const uint32_t d = g.nxt[ri];
                 int64_t pp = pos;
-                if (d == 255) {  // a call longer than 254 positions (never seen): scanned in place
+                if (d == kLongCall) {  // a long call (never seen at 255): scanned in place
                     double v;
                     int32_t q;
                     if (!gamma_scan_call(g, gp, pp, limit, v, q)) break;
